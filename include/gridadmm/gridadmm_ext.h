@@ -1,0 +1,120 @@
+/* gridadmm_ext.h — B200 extensions to the gridadmm C ABI.
+ *
+ * The 23 functions of gridadmm.h are the drop-in boundary.  This header adds
+ * what the reference exposes only as C++ (proj/src/kernels.hpp:70-101,
+ * proj/src/driver.hpp:83-90): a device-resident solver session whose ADMM
+ * state can be read/written in the reference's flat layout
+ * (proj/src/decomp.hpp:64-78) and whose phases can be launched one at a
+ * time.  Parity tests replay a reference state through one phase and compare
+ * bit-for-bit; bench.py times inner iterations with the state resident in
+ * HBM.  All functions are synchronous with respect to the host unless noted;
+ * errors map to gridadmm_status exactly like gridadmm.h.
+ */
+#ifndef GRIDADMM_EXT_H
+#define GRIDADMM_EXT_H
+
+#include "gridadmm.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Host view of one AdmmState (proj/src/decomp.hpp:64-78).  Row vectors have
+ * m = 2G + 8L entries in CouplingLayout order (proj/src/decomp.hpp:32-36);
+ * branch_point is 6 doubles per branch (vi, vj, thi, thj, sij, sji).  Any
+ * pointer may be NULL to skip that array on get/set. */
+typedef struct gridadmm_state_view {
+    double* x;
+    double* xbar;
+    double* z;
+    double* y;
+    double* lambda;
+    double* rho;
+    double* bus_w;        /* num_buses */
+    double* bus_theta;    /* num_buses */
+    double* branch_point; /* 6 * num_branches */
+    double* lt_ij;        /* num_branches */
+    double* lt_ji;        /* num_branches */
+    double* rho_tilde;    /* num_branches */
+    double* beta;         /* scalar */
+} gridadmm_state_view;
+
+typedef struct gridadmm_session gridadmm_session;
+
+/* Phases of one inner iteration, proj/src/driver.cpp:155-176. */
+typedef enum gridadmm_phase {
+    GRIDADMM_PHASE_GENERATORS = 0, /* kernels.cpp:194-209 */
+    GRIDADMM_PHASE_BRANCHES = 1,   /* kernels.cpp:211-292 */
+    GRIDADMM_PHASE_BUSES = 2,      /* kernels.cpp:294-413 */
+    GRIDADMM_PHASE_Z = 3,          /* kernels.cpp:415-422 */
+    GRIDADMM_PHASE_Y = 4,          /* kernels.cpp:424-428 */
+    GRIDADMM_PHASE_OUTER = 5       /* kernels.cpp:430-437 (uses z_inf args) */
+} gridadmm_phase;
+
+/* Number of m rows of the coupling layout (2G + 8L). */
+int gridadmm_network_num_rows(const gridadmm_network* net);
+
+/* Creates a device-resident session for (net, cfg) on the configured device
+ * and loads the cold-start state (proj/src/driver.cpp:26-63). */
+gridadmm_status gridadmm_session_new(const gridadmm_network* net,
+                                     const gridadmm_config* cfg,
+                                     gridadmm_session** out);
+void gridadmm_session_free(gridadmm_session* s);
+
+/* Copies the device state to/from host arrays (synchronous). */
+gridadmm_status gridadmm_session_get_state(const gridadmm_session* s,
+                                           const gridadmm_state_view* v);
+gridadmm_status gridadmm_session_set_state(gridadmm_session* s,
+                                           const gridadmm_state_view* v);
+
+/* Runs one phase on the device state.  For GRIDADMM_PHASE_BRANCHES,
+ * *aux receives the number of branch solve failures; for BUSES, *aux is -1
+ * or the internal index of the first singular bus; for OUTER, aux[0] is
+ * z_inf and aux[1] prev_z_inf (inputs).  aux may be NULL otherwise. */
+gridadmm_status gridadmm_session_phase(gridadmm_session* s, int phase,
+                                       double* aux);
+
+/* Runs up to n inner ADMM iterations of the current outer iteration with the
+ * reference's inner-loop tests (proj/src/driver.cpp:155-220), appending one
+ * record per iteration to records (5 doubles each: primal_res, dual_res,
+ * z_norm, z_drift, branch_failures) when non-NULL.  *done receives the number
+ * of iterations executed; *stop is 0 (ran n), 1 (inner converged / early
+ * exit) or 2 (diverged). */
+gridadmm_status gridadmm_session_iterate(gridadmm_session* s, int n,
+                                         double* records, int* done,
+                                         int* stop);
+
+/* Total device time (ms) of the named kernel class since the session began,
+ * measured with CUDA events on the session stream, and its launch count.
+ * Classes: 0 gen, 1 branch, 2 bus, 3 zy (z+y+residual). */
+gridadmm_status gridadmm_session_kernel_time(const gridadmm_session* s,
+                                             int kernel_class, double* ms,
+                                             long long* launches);
+
+/* Cumulative TRON iterations executed by the branch kernel (lean flop
+ * census input) and branch-kernel launches. */
+gridadmm_status gridadmm_session_counters(const gridadmm_session* s,
+                                          long long* tron_iterations,
+                                          long long* sincos_calls);
+
+/* Number of CUDA devices visible to the library. */
+int gridadmm_device_count(void);
+
+/* Parity probes (test entry points).  Batched TRON (the branch kernel's
+ * trust-region core, proj/src/tron.cpp:228-332) on `count` dense box QPs
+ * f = g'x + x'Hx/2 of dimension n <= 6 (H row-major n*n per problem); x is
+ * the start point in, solution out; status uses TronStatus numbering
+ * (0 converged, 1 iteration limit, 2 numerical error).  And the pinned
+ * device sincos (ga_sincos.h) on n arguments. */
+gridadmm_status gridadmm_probe_tron_qp(int count, int n, const double* h,
+                                       const double* g, const double* l,
+                                       const double* u, double* x, int* status,
+                                       int* iterations);
+gridadmm_status gridadmm_probe_sincos(int n, const double* x, double* s,
+                                      double* c);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GRIDADMM_EXT_H */

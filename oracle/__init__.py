@@ -1,0 +1,208 @@
+"""oracle — TEST INFRASTRUCTURE ONLY (parity checker, never the product).
+
+Two CPU checkers for the ADMM hot path, both pinned to the same sincos as the
+device code (``paper_2110_06879_b200/csrc/ga_sincos.h``):
+
+* ``_ref/libgridadmm_ref.so`` — the UNMODIFIED reference C++ solver
+  (/root/reference/proj/src/*.cpp) compiled in place by ``oracle/Makefile``
+  with ``sincos_shim.c`` and the phase-replay harness ``ref_harness.cpp``.
+  Built in the dev container (where /root/reference exists) and shipped to the
+  GPU box as a prebuilt .so.
+* ``liboracle.so`` — ``gridadmm_oracle.c``, a plain-C restatement of the hot
+  path (generator / branch TRON / bus / z-y / loop control), each function
+  citing the reference line it follows; pinned bit-for-bit against the
+  compiled reference and the golden vectors in ``tests/golden``.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline
+and reference legs may import this package.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import Dict, Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_SO = os.path.join(HERE, "_ref", "libgridadmm_ref.so")
+PORT_SO = os.path.join(HERE, "liboracle.so")
+REF_SRC = "/root/reference/proj/src"
+
+_D = ctypes.c_double
+_DP = ctypes.POINTER(ctypes.c_double)
+_IP = ctypes.POINTER(ctypes.c_int)
+_P = ctypes.c_void_p
+
+STATE_FIELDS = ("x", "xbar", "z", "y", "lambda", "rho", "bus_w", "bus_theta", "branch_point",
+                "lt_ij", "lt_ji", "rho_tilde")
+
+
+class StateView(ctypes.Structure):
+    _fields_ = [(n, _DP) for n in ("x", "xbar", "z", "y", "lambda_", "rho", "bus_w", "bus_theta",
+                                   "branch_point", "lt_ij", "lt_ji", "rho_tilde", "beta")]
+
+
+def build(verbose: bool = False) -> None:
+    """make -C oracle (C restatement always; reference .so when its sources exist)."""
+    out = subprocess.run(["make", "-C", HERE, "-j8"], capture_output=not verbose, text=True)
+    if out.returncode != 0:
+        raise RuntimeError("oracle build failed:\n" + (out.stdout or "") + (out.stderr or ""))
+
+
+def have_ref() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def _dp(a):
+    return None if a is None else a.ctypes.data_as(_DP)
+
+
+def config_vector(rho_pq=10.0, rho_va=1000.0, beta0=1e3, eps=1e-4, inner_tol=0.0, max_outer=20,
+                  max_inner=1000, workers=1, lambda_bound=1e12, beta_max=1e12):
+    """Solver settings in the harness order (ref_harness.cpp config_from)."""
+    return (ctypes.c_double * 10)(rho_pq, rho_va, beta0, eps, inner_tol, max_outer, max_inner,
+                                  workers, lambda_bound, beta_max)
+
+
+def state_shapes(nb, ng, nl):
+    m = 2 * ng + 8 * nl
+    return {"x": m, "xbar": m, "z": m, "y": m, "lambda": m, "rho": m, "bus_w": nb,
+            "bus_theta": nb, "branch_point": 6 * nl, "lt_ij": nl, "lt_ji": nl, "rho_tilde": nl}
+
+
+def make_view(arrays):
+    v = StateView()
+    for f in STATE_FIELDS:
+        a = arrays.get(f)
+        setattr(v, "lambda_" if f == "lambda" else f, _dp(a) if a is not None else None)
+    b = arrays.get("beta")
+    v.beta = _dp(b) if b is not None else None
+    return v
+
+
+class RefLib:
+    """ctypes binding of _ref/libgridadmm_ref.so."""
+
+    _h = None
+
+    @classmethod
+    def get(cls):
+        if cls._h is None:
+            if not have_ref():
+                raise FileNotFoundError(f"{REF_SO} missing; run `make -C oracle` where "
+                                        "/root/reference exists")
+            h = ctypes.CDLL(REF_SO)
+            h.ref_net_load.restype = _P
+            h.ref_net_load.argtypes = [ctypes.c_char_p]
+            h.ref_net_free.argtypes = [_P]
+            h.ref_net_dims.argtypes = [_P, _IP, _IP, _IP, _IP]
+            h.ref_net_export.argtypes = [_P, _DP, _IP, _DP, _IP, _DP, _IP]
+            h.ref_layout_export.argtypes = [_P, _IP, _IP]
+            h.ref_cold_start.argtypes = [_P, _DP, ctypes.POINTER(StateView)]
+            h.ref_phase.restype = ctypes.c_long
+            h.ref_phase.argtypes = [_P, ctypes.c_int, _DP, ctypes.POINTER(StateView), _D, _D]
+            h.ref_solve.argtypes = [_P, _DP, ctypes.POINTER(StateView), ctypes.POINTER(StateView),
+                                    _DP, ctypes.c_int, _IP, _DP]
+            h.ref_tron_qp.argtypes = [ctypes.c_int, ctypes.c_int, _DP, _DP, _DP, _DP, _DP, _IP, _IP]
+            h.ref_last_error.restype = ctypes.c_char_p
+            h.ga_oracle_sincos.argtypes = [_D, _DP, _DP]
+            h.ga_oracle_sincos_batch.argtypes = [ctypes.c_long, _DP, _DP, _DP]
+            cls._h = h
+        return cls._h
+
+
+class RefNet:
+    """A network loaded by the reference's own parser (netdata.cpp:124-237)."""
+
+    def __init__(self, path: str):
+        self.lib = RefLib.get()
+        self.h = self.lib.ref_net_load(os.fsencode(path))
+        if not self.h:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        nb, ng, nl, m = (ctypes.c_int() for _ in range(4))
+        self.lib.ref_net_dims(self.h, ctypes.byref(nb), ctypes.byref(ng), ctypes.byref(nl),
+                              ctypes.byref(m))
+        self.nb, self.ng, self.nl, self.m = nb.value, ng.value, nl.value, m.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.ref_net_free(self.h)
+            self.h = None
+
+    def shapes(self):
+        return state_shapes(self.nb, self.ng, self.nl)
+
+    def empty_state(self) -> Dict[str, np.ndarray]:
+        s = {k: np.zeros(n) for k, n in self.shapes().items()}
+        s["beta"] = np.zeros(1)
+        return s
+
+    def export(self):
+        bus = np.zeros(6 * self.nb)
+        ids = np.zeros(self.nb, dtype=np.int32)
+        gen = np.zeros(8 * self.ng)
+        ends = np.zeros(2 * self.nl, dtype=np.int32)
+        br = np.zeros(14 * self.nl)
+        ref = ctypes.c_int()
+        self.lib.ref_net_export(self.h, _dp(bus), ids.ctypes.data_as(_IP), _dp(gen),
+                                ends.ctypes.data_as(_IP), _dp(br), ctypes.byref(ref))
+        return {"bus": bus.reshape(-1, 6), "bus_id": ids, "gen": gen.reshape(-1, 8),
+                "ends": ends.reshape(-1, 2), "branch": br.reshape(-1, 14), "ref_bus": ref.value}
+
+    def layout(self):
+        counts = np.zeros(6 * self.nb, dtype=np.int32)
+        rows = np.zeros(max(self.m, 1), dtype=np.int32)
+        self.lib.ref_layout_export(self.h, counts.ctypes.data_as(_IP), rows.ctypes.data_as(_IP))
+        return counts.reshape(-1, 6), rows[: self.m]
+
+    def cold_start(self, **cfg) -> Dict[str, np.ndarray]:
+        s = self.empty_state()
+        v = make_view(s)
+        self.lib.ref_cold_start(self.h, config_vector(**cfg), ctypes.byref(v))
+        return s
+
+    def phase(self, phase: int, state: Dict[str, np.ndarray], z_inf=0.0, prev_z_inf=-1.0,
+              **cfg) -> int:
+        """Runs one reference phase on `state` in place (kernels.hpp:70-101)."""
+        v = make_view(state)
+        return int(self.lib.ref_phase(self.h, phase, config_vector(**cfg), ctypes.byref(v),
+                                      z_inf, prev_z_inf))
+
+    def solve(self, init: Optional[Dict[str, np.ndarray]] = None, cap: int = 100000, **cfg):
+        """Full reference solve; returns (series[n, 5], info[9], final_state)."""
+        series = np.zeros(5 * cap)
+        n = ctypes.c_int()
+        info = np.zeros(9)
+        fin = self.empty_state()
+        vf = make_view(fin)
+        vi = make_view(init) if init is not None else None
+        rc = self.lib.ref_solve(self.h, config_vector(**cfg),
+                                ctypes.byref(vi) if vi is not None else None, ctypes.byref(vf),
+                                _dp(series), cap, ctypes.byref(n), _dp(info))
+        if rc != 0:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        k = min(n.value, cap)
+        return series[: 5 * k].reshape(-1, 5), info, fin
+
+
+def ref_tron_qp(H, g, lo, hi, x0):
+    lib = RefLib.get()
+    count, n = g.shape
+    x = np.ascontiguousarray(x0, dtype=np.float64).copy()
+    st = np.zeros(count, dtype=np.int32)
+    its = np.zeros(count, dtype=np.int32)
+    args = [np.ascontiguousarray(a, dtype=np.float64) for a in (H, g, lo, hi)]
+    lib.ref_tron_qp(count, n, *[_dp(a) for a in args], _dp(x), st.ctypes.data_as(_IP),
+                    its.ctypes.data_as(_IP))
+    return x, st, its
+
+
+def ref_sincos(x):
+    lib = RefLib.get()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    s = np.zeros_like(x)
+    c = np.zeros_like(x)
+    lib.ga_oracle_sincos_batch(x.size, _dp(x), _dp(s), _dp(c))
+    return s, c

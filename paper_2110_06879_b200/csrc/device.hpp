@@ -1,0 +1,104 @@
+// device.hpp — HBM-resident layout of one network + ADMM state, and the
+// extern "C"-style launchers the host driver calls (one per phase).
+//
+// Layout (all FP64 unless noted, SoA, 256-B aligned allocations):
+//   rows   m = 2G + 8L in the reference's CouplingLayout order
+//          (proj/src/decomp.hpp:32-36): gen g -> rows 2g, 2g+1; branch b ->
+//          rows 2G + 8b + k, k in (pij, qij, pji, qji, wi, thi, wj, thj).
+//          x, xbar, z, y, lambda, rho: 6 m-vectors.
+//   branch L: ends (int32 from/to), 8 admittance coefficients [k*L + b],
+//          rate, point [k*L + b] (k < 6), lt_ij, lt_ji, rho_tilde.
+//   bus    N: pd, qd, gs, bs, vmin, vmax, w, theta; a CSR of the m rows by
+//          owning bus, each bus's rows grouped as
+//          [w | theta | gen_p | gen_q | flow_p | flow_q] in the reference's
+//          per-group order (proj/src/decomp.cpp:7-31); grp[7*i + k] are the
+//          group start offsets (k = 0..6, last = end).
+//   gen    G: pmin, pmax, qmin, qmax, c2, c1.
+#ifndef GA_DEVICE_HPP
+#define GA_DEVICE_HPP
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace ga {
+
+struct DevNet {
+    int nb = 0, ng = 0, nl = 0, m = 0;
+    int ref_bus = -1;
+    // generators
+    double *g_pmin = nullptr, *g_pmax = nullptr, *g_qmin = nullptr, *g_qmax = nullptr;
+    double *g_c2 = nullptr, *g_c1 = nullptr;
+    // branches
+    int *br_from = nullptr, *br_to = nullptr;
+    double* br_y = nullptr;     // [8][nl]: gii bii gij bij gji bji gjj bjj
+    double* br_rate = nullptr;  // [nl], 0 = unlimited
+    int* lim_list = nullptr;    // indices of rate-limited branches
+    int* unl_list = nullptr;    // indices of unlimited branches
+    int n_lim = 0, n_unl = 0;
+    // buses
+    double *b_pd = nullptr, *b_qd = nullptr, *b_gs = nullptr, *b_bs = nullptr;
+    double *b_vmin = nullptr, *b_vmax = nullptr;
+    int* bus_grp = nullptr;   // [7*nb] group offsets into bus_rows
+    int* bus_rows = nullptr;  // [m]
+};
+
+struct DevState {
+    double *x = nullptr, *xbar = nullptr, *z = nullptr, *y = nullptr;
+    double *lambda = nullptr, *rho = nullptr;
+    double *bus_w = nullptr, *bus_theta = nullptr;
+    double* bp = nullptr;  // [6][nl]
+    double *lt_ij = nullptr, *lt_ji = nullptr, *rho_t = nullptr;
+};
+
+// Per-iteration scalars reduced on the device.  Maxima of non-negative
+// doubles are kept as their IEEE bit patterns (order-preserving as uint64).
+struct DevScalars {
+    unsigned long long primal_inf;  // max |x - xbar + z|
+    unsigned long long dual_inf;    // max |xbar - xbar_prev| (times rho_max on host)
+    unsigned long long z_inf;       // max |z|
+    unsigned long long z_drift;     // max |z - z_prev|
+    unsigned long long failures;    // branch NumericalError count
+    unsigned long long tron_iters;  // TRON iterations executed (census)
+    unsigned long long sincos;      // sincos evaluations (census)
+    int singular_bus;               // min singular bus index, INT_MAX if none
+    int pad;
+};
+
+struct BranchCfg {
+    double gtol = 1e-6;
+    int max_iterations = 200;
+    double cg_tol = 0.1;
+    int max_cg = 32;
+    double delta_floor = 1e-3;
+    double limit_tighten = 0.99;
+};
+
+// ---- launchers (kernels.cu / branch.cu) ----------------------------------
+void launch_generators(const DevNet& n, const DevState& s, cudaStream_t st);
+void launch_branches(const DevNet& n, const DevState& s, const BranchCfg& cfg,
+                     DevScalars* sc, cudaStream_t st);
+void launch_buses(const DevNet& n, const DevState& s, DevScalars* sc, cudaStream_t st);
+// z update + y update + residual/z norms, fused (one pass over m).
+void launch_zy(const DevNet& n, const DevState& s, double beta, DevScalars* sc,
+               cudaStream_t st);
+// Separate z / y phases (phase-replay API).
+void launch_z_only(const DevNet& n, const DevState& s, double beta, cudaStream_t st);
+void launch_y_only(const DevNet& n, const DevState& s, cudaStream_t st);
+void launch_outer(const DevNet& n, const DevState& s, double beta, double lam_min,
+                  double lam_max, cudaStream_t st);
+void launch_reset_scalars(DevScalars* sc, cudaStream_t st);
+// max(0, max_k v[k]) with NaN skipped (driver.cpp:179-183 rho_max), as bits.
+void launch_rowmax(const double* v, int n, unsigned long long* dst, cudaStream_t st);
+// Tracking carry-over: clamp x/xbar p-rows into [pmin, pmax] (tracking.cpp:65-70).
+void launch_clamp_gen_p(const DevNet& n, const DevState& s, cudaStream_t st);
+// Batched TRON on dense box QPs (parity test of the TRON core).
+void launch_tron_qp(int count, int n, const double* h, const double* g,
+                    const double* l, const double* u, double* x, int* status,
+                    int* iterations, cudaStream_t st);
+// Pinned sincos on the device (parity probe).
+void launch_sincos_probe(const double* x, double* s, double* c, int n, cudaStream_t st);
+
+}  // namespace ga
+
+#endif

@@ -1,0 +1,377 @@
+// kernels.cu — the HBM-bound phases of one inner ADMM iteration:
+//   generator projection (north-star (a), kernels.cpp:194-209),
+//   bus consensus QP      (north-star (c), kernels.cpp:294-413),
+//   fused z / y / residual norms (north-star (d), kernels.cpp:415-428 +
+//   decomp.cpp:59-72 + driver.cpp:179-186,213-215),
+//   outer multiplier update (kernels.cpp:430-437),
+//   tracking carry-over clamp (tracking.cpp:65-70).
+// All arithmetic mirrors the reference's expression trees (compiled with
+// -fmad=false); the infinity-norm reductions are order-free maxima, so a
+// warp+grid reduction gives the reference's bits exactly.
+#include <climits>
+
+#include "device.hpp"
+#include "ga_math.h"
+
+namespace ga {
+
+namespace {
+
+constexpr int kBlock = 256;
+
+__device__ __forceinline__ unsigned long long dbits(double v) {
+    return static_cast<unsigned long long>(__double_as_longlong(v));
+}
+
+// Block-wide max of non-negative doubles, then one atomicMax per block on the
+// IEEE bit pattern (monotone for non-negative values).
+template <int NV>
+__device__ __forceinline__ void block_max_atomic(double (&v)[NV], unsigned long long* const (&dst)[NV]) {
+    __shared__ double red[NV][kBlock / 32];
+    const unsigned full = 0xffffffffu;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[q] = fmax(v[q], __shfl_down_sync(full, v[q], o));
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) red[q][wid] = v[q];
+    }
+    __syncthreads();
+    if (wid == 0) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            double t = lane < (int)(blockDim.x >> 5) ? red[q][lane] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t = fmax(t, __shfl_down_sync(full, t, o));
+            if (lane == 0 && t > 0.0) atomicMax(dst[q], dbits(t));
+        }
+    }
+}
+
+// ---- generators (kernels.cpp:194-209) ----------------------------------
+__global__ void __launch_bounds__(kBlock) gen_kernel(DevNet n, DevState s) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n.ng) return;
+    // rows 2g, 2g+1 are adjacent: one 16-B load per array
+    const double2 xb = reinterpret_cast<const double2*>(s.xbar)[g];
+    const double2 zz = reinterpret_cast<const double2*>(s.z)[g];
+    const double2 yy = reinterpret_cast<const double2*>(s.y)[g];
+    const double2 rr = reinterpret_cast<const double2*>(s.rho)[g];
+    const double p = (rr.x * (xb.x - zz.x) - yy.x - n.g_c1[g]) / (2.0 * n.g_c2[g] + rr.x);
+    const double q = (rr.y * (xb.y - zz.y) - yy.y) / rr.y;
+    double2 out;
+    out.x = sclamp(p, n.g_pmin[g], n.g_pmax[g]);
+    out.y = sclamp(q, n.g_qmin[g], n.g_qmax[g]);
+    reinterpret_cast<double2*>(s.x)[g] = out;
+}
+
+// ---- buses (kernels.cpp:294-413) ----------------------------------------
+// One thread per bus.  Variables: [0] w, [1] theta, then one duplicate per
+// row in gen_p, gen_q, flow_p, flow_q order.  A's entries are implied by the
+// group of each column.  Sums run over columns in the reference's order;
+// columns whose A entry is an exact zero are skipped when every c is finite
+// (the skipped term is a signed zero added to an accumulator that started
+// at +0.0 — exact), otherwise the dense loop is used.
+__device__ __forceinline__ double a_coef(int r, int grp, double gs, double bs, bool ref) {
+    // grp: 0 = w, 1 = theta, 2 = gen_p, 3 = gen_q, 4 = flow_p, 5 = flow_q
+    switch (r) {
+        case 0: return grp == 0 ? -gs : grp == 2 ? 1.0 : grp == 4 ? -1.0 : 0.0;
+        case 1: return grp == 0 ? bs : grp == 3 ? 1.0 : grp == 5 ? -1.0 : 0.0;
+        default: return (ref && grp == 1) ? 1.0 : 0.0;
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) bus_kernel(DevNet n, DevState s, DevScalars* sc) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double dual = 0.0;
+    if (i < n.nb) {
+        const int* grp = n.bus_grp + 7 * i;
+        const int* rows = n.bus_rows;
+        const bool ref = i == n.ref_bus;
+        const double gs = n.b_gs[i], bs = n.b_bs[i];
+        auto cval = [&](int row) { return s.rho[row] * (s.x[row] + s.z[row]) + s.y[row]; };
+
+        double q0 = 0.0, c0 = 0.0, q1 = 0.0, c1 = 0.0;
+        for (int k = grp[0]; k < grp[1]; ++k) {
+            const int row = rows[k];
+            q0 += s.rho[row];
+            c0 += cval(row);
+        }
+        for (int k = grp[1]; k < grp[2]; ++k) {
+            const int row = rows[k];
+            q1 += s.rho[row];
+            c1 += cval(row);
+        }
+        if (q0 == 0.0) q0 = 1.0;
+        if (q1 == 0.0) q1 = 1.0;
+        const int nc = ref ? 3 : 2;
+
+        // finiteness of every c decides the sparse (exact) vs dense path
+        bool finite = sfinite(c0) && sfinite(c1);
+        for (int k = grp[2]; k < grp[6] && finite; ++k) finite = sfinite(cval(rows[k]));
+
+        double S[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, rhs[3] = {0, 0, 0};
+        const double bvec[3] = {n.b_pd[i], n.b_qd[i], 0.0};
+        if (finite) {
+            const double a00 = -gs, a10 = bs;
+            double s00 = 0.0, s01 = 0.0, s11 = 0.0, s22 = 0.0, r0 = 0.0, r1 = 0.0, r2 = 0.0;
+            // column 0 (w)
+            s00 += a00 * a00 / q0;
+            s01 += a00 * a10 / q0;
+            s11 += a10 * a10 / q0;
+            r0 += a00 * c0 / q0;
+            r1 += a10 * c0 / q0;
+            // column 1 (theta): only the REF row is non-zero
+            if (ref) {
+                s22 += 1.0 * 1.0 / q1;
+                r2 += 1.0 * c1 / q1;
+            }
+            // S[0][0] / rhs[0]: gen_p then flow_p columns (+1 / -1)
+            for (int k = grp[2]; k < grp[3]; ++k) {
+                const int row = rows[k];
+                const double q = s.rho[row];
+                s00 += 1.0 * 1.0 / q;
+                r0 += 1.0 * cval(row) / q;
+            }
+            for (int k = grp[4]; k < grp[5]; ++k) {
+                const int row = rows[k];
+                const double q = s.rho[row];
+                s00 += -1.0 * -1.0 / q;
+                r0 += -1.0 * cval(row) / q;
+            }
+            // S[1][1] / rhs[1]: gen_q then flow_q columns
+            for (int k = grp[3]; k < grp[4]; ++k) {
+                const int row = rows[k];
+                const double q = s.rho[row];
+                s11 += 1.0 * 1.0 / q;
+                r1 += 1.0 * cval(row) / q;
+            }
+            for (int k = grp[5]; k < grp[6]; ++k) {
+                const int row = rows[k];
+                const double q = s.rho[row];
+                s11 += -1.0 * -1.0 / q;
+                r1 += -1.0 * cval(row) / q;
+            }
+            // S[1][0] = 0 + bs*(-gs)/q0: commutative product, same bits as s01
+            S[0] = s00; S[1] = s01; S[3] = s01; S[4] = s11;
+            S[8] = s22;
+            rhs[0] = r0 - bvec[0];
+            rhs[1] = r1 - bvec[1];
+            rhs[2] = r2 - bvec[2];
+        } else {
+            // dense reference loop (kernels.cpp:350-361), any column value
+            auto col = [&](int j, int* g, double* qj, double* cj) {
+                if (j == 0) { *g = 0; *qj = q0; *cj = c0; return; }
+                if (j == 1) { *g = 1; *qj = q1; *cj = c1; return; }
+                const int k = grp[2] + (j - 2);
+                int gg = 2;
+                while (k >= grp[gg + 1]) ++gg;
+                const int row = rows[k];
+                *g = gg;
+                *qj = s.rho[row];
+                *cj = cval(row);
+            };
+            const int nv = 2 + (grp[6] - grp[2]);
+            for (int r = 0; r < nc; ++r) {
+                for (int t = 0; t < nc; ++t) {
+                    double acc = 0.0;
+                    for (int j = 0; j < nv; ++j) {
+                        int g; double qj, cj;
+                        col(j, &g, &qj, &cj);
+                        acc += a_coef(r, g, gs, bs, ref) * a_coef(t, g, gs, bs, ref) / qj;
+                    }
+                    S[r * 3 + t] = acc;
+                }
+                double acc = 0.0;
+                for (int j = 0; j < nv; ++j) {
+                    int g; double qj, cj;
+                    col(j, &g, &qj, &cj);
+                    acc += a_coef(r, g, gs, bs, ref) * cj / qj;
+                }
+                rhs[r] = acc - bvec[r];
+            }
+        }
+
+        // Gaussian elimination with partial pivoting (kernels.cpp:364-391)
+        double mu[3] = {0, 0, 0};
+        bool singular = false;
+        {
+            int piv[3] = {0, 1, 2};
+            for (int col = 0; col < nc && !singular; ++col) {
+                int best = col;
+                for (int r = col + 1; r < nc; ++r)
+                    if (fabs(S[piv[r] * 3 + col]) > fabs(S[piv[best] * 3 + col])) best = r;
+                const int tmp = piv[col]; piv[col] = piv[best]; piv[best] = tmp;
+                const double d = S[piv[col] * 3 + col];
+                if (fabs(d) < 1e-14) { singular = true; break; }
+                for (int r = col + 1; r < nc; ++r) {
+                    const double f = S[piv[r] * 3 + col] / d;
+                    for (int s2 = col; s2 < nc; ++s2) S[piv[r] * 3 + s2] -= f * S[piv[col] * 3 + s2];
+                    rhs[piv[r]] -= f * rhs[piv[col]];
+                }
+            }
+            if (!singular) {
+                for (int col = nc - 1; col >= 0; --col) {
+                    double acc = rhs[piv[col]];
+                    for (int s2 = col + 1; s2 < nc; ++s2) acc -= S[piv[col] * 3 + s2] * mu[s2];
+                    mu[col] = acc / S[piv[col] * 3 + col];
+                }
+            }
+        }
+        if (singular) {
+            atomicMin(&sc->singular_bus, i);
+        } else {
+            // xbar = Q^-1 (c - A' mu) (kernels.cpp:394-399), dense in r
+            auto solve_col = [&](int g, double cj, double qj) {
+                double acc = cj;
+                for (int r = 0; r < nc; ++r) acc -= a_coef(r, g, gs, bs, ref) * mu[r];
+                return acc / qj;
+            };
+            const double w = solve_col(0, c0, q0);
+            const double th = solve_col(1, c1, q1);
+            s.bus_w[i] = w;
+            s.bus_theta[i] = th;
+            for (int k = grp[0]; k < grp[1]; ++k) {
+                const int row = rows[k];
+                dual = smax(dual, abs_or_zero(w - s.xbar[row]));
+                s.xbar[row] = w;
+            }
+            for (int k = grp[1]; k < grp[2]; ++k) {
+                const int row = rows[k];
+                dual = smax(dual, abs_or_zero(th - s.xbar[row]));
+                s.xbar[row] = th;
+            }
+            for (int gg = 2; gg < 6; ++gg)
+                for (int k = grp[gg]; k < grp[gg + 1]; ++k) {
+                    const int row = rows[k];
+                    const double v = solve_col(gg, cval(row), s.rho[row]);
+                    dual = smax(dual, abs_or_zero(v - s.xbar[row]));
+                    s.xbar[row] = v;
+                }
+        }
+    }
+    double vals[1] = {dual};
+    unsigned long long* const dst[1] = {&sc->dual_inf};
+    block_max_atomic<1>(vals, dst);
+}
+
+// ---- fused z / y / residual (kernels.cpp:415-428, decomp.cpp:59-72) -----
+__global__ void __launch_bounds__(kBlock) zy_kernel(DevNet n, DevState s, double beta,
+                                                    DevScalars* sc) {
+    double pr = 0.0, zi = 0.0, zd = 0.0;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n.m; k += gridDim.x * blockDim.x) {
+        const double x = s.x[k], xb = s.xbar[k], rho = s.rho[k];
+        const double zold = s.z[k], y = s.y[k];
+        const double r = x - xb;
+        const double z = -(s.lambda[k] + y + rho * r) / (rho + beta);
+        const double res = x - xb + z;
+        s.z[k] = z;
+        s.y[k] = y + rho * res;
+        pr = smax(pr, abs_or_zero(res));
+        zi = smax(zi, abs_or_zero(z));
+        zd = smax(zd, abs_or_zero(z - zold));
+    }
+    double vals[3] = {pr, zi, zd};
+    unsigned long long* const dst[3] = {&sc->primal_inf, &sc->z_inf, &sc->z_drift};
+    block_max_atomic<3>(vals, dst);
+}
+
+__global__ void z_only_kernel(DevNet n, DevState s, double beta) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n.m) return;
+    const double r = s.x[k] - s.xbar[k];
+    s.z[k] = -(s.lambda[k] + s.y[k] + s.rho[k] * r) / (s.rho[k] + beta);
+}
+
+__global__ void y_only_kernel(DevNet n, DevState s) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n.m) return;
+    s.y[k] += s.rho[k] * (s.x[k] - s.xbar[k] + s.z[k]);
+}
+
+__global__ void outer_kernel(DevNet n, DevState s, double beta, double lmin, double lmax) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n.m) return;
+    s.lambda[k] = sclamp(s.lambda[k] + beta * s.z[k], lmin, lmax);
+}
+
+__global__ void clamp_gen_p_kernel(DevNet n, DevState s) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n.ng) return;
+    const int pr = 2 * g;
+    s.x[pr] = sclamp(s.x[pr], n.g_pmin[g], n.g_pmax[g]);
+    s.xbar[pr] = sclamp(s.xbar[pr], n.g_pmin[g], n.g_pmax[g]);
+}
+
+__global__ void __launch_bounds__(kBlock) rowmax_kernel(const double* v, int n,
+                                                        unsigned long long* dst) {
+    double mx = 0.0;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        mx = smax(mx, v[k]);
+    double vals[1] = {mx};
+    unsigned long long* const d[1] = {dst};
+    block_max_atomic<1>(vals, d);
+}
+
+__global__ void reset_scalars_kernel(DevScalars* sc) {
+    sc->primal_inf = 0;
+    sc->dual_inf = 0;
+    sc->z_inf = 0;
+    sc->z_drift = 0;
+    sc->failures = 0;
+    sc->singular_bus = INT_MAX;
+}
+
+inline int blocks_for(int n) { return (n + kBlock - 1) / kBlock; }
+
+}  // namespace
+
+void launch_generators(const DevNet& n, const DevState& s, cudaStream_t st) {
+    if (n.ng > 0) gen_kernel<<<blocks_for(n.ng), kBlock, 0, st>>>(n, s);
+}
+
+void launch_buses(const DevNet& n, const DevState& s, DevScalars* sc, cudaStream_t st) {
+    if (n.nb > 0) bus_kernel<<<blocks_for(n.nb), kBlock, 0, st>>>(n, s, sc);
+}
+
+void launch_zy(const DevNet& n, const DevState& s, double beta, DevScalars* sc,
+               cudaStream_t st) {
+    if (n.m <= 0) return;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int blocks = blocks_for(n.m);
+    if (blocks > sms * 8) blocks = sms * 8;
+    zy_kernel<<<blocks, kBlock, 0, st>>>(n, s, beta, sc);
+}
+
+void launch_z_only(const DevNet& n, const DevState& s, double beta, cudaStream_t st) {
+    if (n.m > 0) z_only_kernel<<<blocks_for(n.m), kBlock, 0, st>>>(n, s, beta);
+}
+
+void launch_y_only(const DevNet& n, const DevState& s, cudaStream_t st) {
+    if (n.m > 0) y_only_kernel<<<blocks_for(n.m), kBlock, 0, st>>>(n, s);
+}
+
+void launch_outer(const DevNet& n, const DevState& s, double beta, double lmin, double lmax,
+                  cudaStream_t st) {
+    if (n.m > 0) outer_kernel<<<blocks_for(n.m), kBlock, 0, st>>>(n, s, beta, lmin, lmax);
+}
+
+void launch_clamp_gen_p(const DevNet& n, const DevState& s, cudaStream_t st) {
+    if (n.ng > 0) clamp_gen_p_kernel<<<blocks_for(n.ng), kBlock, 0, st>>>(n, s);
+}
+
+void launch_rowmax(const double* v, int n, unsigned long long* dst, cudaStream_t st) {
+    cudaMemsetAsync(dst, 0, sizeof(unsigned long long), st);
+    if (n > 0) rowmax_kernel<<<64, kBlock, 0, st>>>(v, n, dst);
+}
+
+void launch_reset_scalars(DevScalars* sc, cudaStream_t st) {
+    reset_scalars_kernel<<<1, 1, 0, st>>>(sc);
+}
+
+}  // namespace ga

@@ -1,0 +1,81 @@
+// network.hpp — host-side power network model, MATPOWER reader and the
+// coupling layout that fixes the device row order.
+//
+// Semantics follow the reference (proj/src/netdata.{hpp,cpp},
+// proj/src/decomp.{hpp,cpp}): identical indexing (file order, status-0
+// generators/branches dropped), per-unit conversion, admittances of the
+// pi-model with complex tap.  The parse itself is new code (single pass over
+// the text, strtod tokens).
+#ifndef GA_NETWORK_HPP
+#define GA_NETWORK_HPP
+
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+namespace ga {
+
+class ParseError : public std::runtime_error {
+public:
+    explicit ParseError(const std::string& w) : std::runtime_error(w) {}
+};
+
+struct Bus {
+    int id = 0;
+    int type = 1;  // 1 PQ, 2 PV, 3 REF
+    double pd = 0, qd = 0, gs = 0, bs = 0, vmin = 0, vmax = 0;
+};
+
+struct Gen {
+    int bus = 0;
+    double pmin = 0, pmax = 0, qmin = 0, qmax = 0;
+    double c2 = 0, c1 = 0, c0 = 0;
+};
+
+// gii bii gij bij gji bji gjj bjj (netdata.hpp:37-43)
+struct Admittance {
+    double c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+};
+
+struct Line {
+    int from = 0, to = 0;
+    double r = 0, x = 0, b = 0, tap = 1, shift = 0, rate = 0;
+    Admittance y;
+    bool limited() const { return rate > 0.0; }
+};
+
+struct Network {
+    double base_mva = 100.0;
+    std::vector<Bus> buses;
+    std::vector<Gen> gens;
+    std::vector<Line> lines;
+    std::unordered_map<int, int> bus_index;
+    int ref_bus = -1;
+
+    int nb() const { return static_cast<int>(buses.size()); }
+    int ng() const { return static_cast<int>(gens.size()); }
+    int nl() const { return static_cast<int>(lines.size()); }
+    int m() const { return 2 * ng() + 8 * nl(); }
+};
+
+Admittance derive_admittance(double r, double x, double b, double tap, double shift);
+// pij, qij, pji, qji at a voltage point (netdata.cpp:33-45), pinned sincos.
+void branch_flows_host(const Admittance& y, double vi, double vj, double thi, double thj,
+                       double out[4]);
+
+Network parse_matpower(const std::string& text);
+Network load_matpower(const std::string& path);
+
+// Bus-owned row CSR in the reference's CouplingLayout order
+// (decomp.cpp:7-31): per bus, groups [w | theta | gen_p | gen_q | flow_p |
+// flow_q]; grp has 7 offsets per bus.
+struct BusCsr {
+    std::vector<int> grp;   // 7 * nb
+    std::vector<int> rows;  // m
+};
+BusCsr build_bus_csr(const Network& net);
+
+}  // namespace ga
+
+#endif

@@ -1,0 +1,372 @@
+// session.cpp — device residency of one network + AdmmState and the phase
+// sequence of one inner iteration (proj/src/driver.cpp:155-186).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "ga_math.h"
+#include "solver.hpp"
+
+namespace ga {
+
+namespace {
+
+void check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+double from_bits(unsigned long long b) {
+    double v;
+    std::memcpy(&v, &b, sizeof v);
+    return v;
+}
+
+}  // namespace
+
+double SolverConfig::effective_inner_tol(int m) const {
+    return inner_tol > 0.0 ? inner_tol : eps * std::sqrt(static_cast<double>(m));
+}
+
+Session::Session(const Network& net, const SolverConfig& cfg) : net_(net), cfg_(cfg) {
+    check(cudaSetDevice(cfg.device), "cudaSetDevice");
+    check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (auto& e : ev_) check(cudaEventCreate(&e), "cudaEventCreate");
+    try {
+        upload_network();
+        check(cudaMalloc(&sc_, sizeof(DevScalars)), "cudaMalloc scalars");
+        check(cudaMemset(sc_, 0, sizeof(DevScalars)), "cudaMemset scalars");
+        check(cudaMallocHost(&sc_host_, sizeof(DevScalars)), "cudaMallocHost");
+        check(cudaMalloc(&red_, sizeof(unsigned long long)), "cudaMalloc red");
+    } catch (...) {
+        free_all();
+        throw;
+    }
+    beta_ = cfg.beta0;
+}
+
+Session::~Session() { free_all(); }
+
+void Session::free_all() {
+    if (stream_) cudaStreamSynchronize(stream_);
+    for (void* p : allocs_) cudaFree(p);
+    allocs_.clear();
+    if (sc_) cudaFree(sc_);
+    if (red_) cudaFree(red_);
+    if (sc_host_) cudaFreeHost(sc_host_);
+    sc_ = nullptr;
+    red_ = nullptr;
+    sc_host_ = nullptr;
+    for (auto& e : ev_)
+        if (e) cudaEventDestroy(e);
+    if (stream_) cudaStreamDestroy(stream_);
+    stream_ = nullptr;
+}
+
+void Session::upload_network() {
+    const int nb = net_.nb(), ng = net_.ng(), nl = net_.nl(), m = net_.m();
+    dn_.nb = nb;
+    dn_.ng = ng;
+    dn_.nl = nl;
+    dn_.m = m;
+    dn_.ref_bus = net_.ref_bus;
+    auto alloc = [&](auto*& p, size_t count) {
+        using T = std::remove_reference_t<decltype(*p)>;
+        void* raw = nullptr;
+        check(cudaMalloc(&raw, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+        allocs_.push_back(raw);
+        p = static_cast<T*>(raw);
+    };
+    auto put = [&](auto* dst, const auto& host) {
+        if (!host.empty())
+            check(cudaMemcpy(dst, host.data(), host.size() * sizeof(host[0]), cudaMemcpyHostToDevice),
+                  "cudaMemcpy H2D");
+    };
+    // generators
+    std::vector<double> pmin(ng), pmax(ng), qmin(ng), qmax(ng), c2(ng), c1(ng);
+    for (int g = 0; g < ng; ++g) {
+        const Gen& x = net_.gens[g];
+        pmin[g] = x.pmin; pmax[g] = x.pmax; qmin[g] = x.qmin; qmax[g] = x.qmax;
+        c2[g] = x.c2; c1[g] = x.c1;
+    }
+    alloc(dn_.g_pmin, ng); put(dn_.g_pmin, pmin);
+    alloc(dn_.g_pmax, ng); put(dn_.g_pmax, pmax);
+    alloc(dn_.g_qmin, ng); put(dn_.g_qmin, qmin);
+    alloc(dn_.g_qmax, ng); put(dn_.g_qmax, qmax);
+    alloc(dn_.g_c2, ng); put(dn_.g_c2, c2);
+    alloc(dn_.g_c1, ng); put(dn_.g_c1, c1);
+    // branches
+    std::vector<int> from(nl), to(nl), lim, unl;
+    std::vector<double> yc(8 * static_cast<size_t>(nl)), rate(nl);
+    for (int b = 0; b < nl; ++b) {
+        const Line& l = net_.lines[b];
+        from[b] = l.from;
+        to[b] = l.to;
+        rate[b] = l.rate;
+        for (int k = 0; k < 8; ++k) yc[static_cast<size_t>(k) * nl + b] = l.y.c[k];
+        (l.limited() ? lim : unl).push_back(b);
+    }
+    alloc(dn_.br_from, nl); put(dn_.br_from, from);
+    alloc(dn_.br_to, nl); put(dn_.br_to, to);
+    alloc(dn_.br_y, 8 * static_cast<size_t>(nl)); put(dn_.br_y, yc);
+    alloc(dn_.br_rate, nl); put(dn_.br_rate, rate);
+    alloc(dn_.lim_list, lim.size()); put(dn_.lim_list, lim);
+    alloc(dn_.unl_list, unl.size()); put(dn_.unl_list, unl);
+    dn_.n_lim = static_cast<int>(lim.size());
+    dn_.n_unl = static_cast<int>(unl.size());
+    // buses
+    std::vector<double> pd(nb), qd(nb), gs(nb), bs(nb), vmin(nb), vmax(nb);
+    for (int i = 0; i < nb; ++i) {
+        const Bus& b = net_.buses[i];
+        pd[i] = b.pd; qd[i] = b.qd; gs[i] = b.gs; bs[i] = b.bs; vmin[i] = b.vmin; vmax[i] = b.vmax;
+    }
+    alloc(dn_.b_pd, nb); put(dn_.b_pd, pd);
+    alloc(dn_.b_qd, nb); put(dn_.b_qd, qd);
+    alloc(dn_.b_gs, nb); put(dn_.b_gs, gs);
+    alloc(dn_.b_bs, nb); put(dn_.b_bs, bs);
+    alloc(dn_.b_vmin, nb); put(dn_.b_vmin, vmin);
+    alloc(dn_.b_vmax, nb); put(dn_.b_vmax, vmax);
+    const BusCsr csr = build_bus_csr(net_);
+    alloc(dn_.bus_grp, csr.grp.size()); put(dn_.bus_grp, csr.grp);
+    alloc(dn_.bus_rows, csr.rows.size()); put(dn_.bus_rows, csr.rows);
+    // state
+    alloc(ds_.x, m); alloc(ds_.xbar, m); alloc(ds_.z, m); alloc(ds_.y, m);
+    alloc(ds_.lambda, m); alloc(ds_.rho, m);
+    alloc(ds_.bus_w, nb); alloc(ds_.bus_theta, nb);
+    alloc(ds_.bp, 6 * static_cast<size_t>(nl));
+    alloc(ds_.lt_ij, nl); alloc(ds_.lt_ji, nl); alloc(ds_.rho_t, nl);
+}
+
+// make_state + cold_start (decomp.cpp:37-57, driver.cpp:26-63), on the host
+// (O(G + L), once per solve) then one upload.
+void Session::cold_start() {
+    const int nb = net_.nb(), ng = net_.ng(), nl = net_.nl(), m = net_.m();
+    HostState s;
+    s.x.assign(m, 0.0);
+    s.xbar.assign(m, 0.0);
+    s.z.assign(m, 0.0);
+    s.y.assign(m, 0.0);
+    s.lambda.assign(m, 0.0);
+    s.rho.resize(m);
+    for (int k = 0; k < m; ++k) {
+        const bool pq = k < 2 * ng || (k - 2 * ng) % 8 < 4;
+        s.rho[k] = pq ? cfg_.rho_pq : cfg_.rho_va;
+    }
+    s.beta = cfg_.beta0;
+    s.bus_w.assign(nb, 0.0);
+    s.bus_theta.assign(nb, 0.0);
+    s.bp.assign(6 * static_cast<size_t>(nl), 0.0);
+    s.lt_ij.assign(nl, 0.0);
+    s.lt_ji.assign(nl, 0.0);
+    s.rho_t.assign(nl, cfg_.rho_pq);
+    for (int g = 0; g < ng; ++g) {
+        const Gen& gen = net_.gens[g];
+        s.x[2 * g] = s.xbar[2 * g] = 0.5 * (gen.pmin + gen.pmax);
+        s.x[2 * g + 1] = s.xbar[2 * g + 1] = 0.5 * (gen.qmin + gen.qmax);
+    }
+    for (int i = 0; i < nb; ++i) {
+        const double v = 0.5 * (net_.buses[i].vmin + net_.buses[i].vmax);
+        s.bus_w[i] = v * v;
+        s.bus_theta[i] = 0.0;
+    }
+    for (int b = 0; b < nl; ++b) {
+        const Line& br = net_.lines[b];
+        const double vi = 0.5 * (net_.buses[br.from].vmin + net_.buses[br.from].vmax);
+        const double vj = 0.5 * (net_.buses[br.to].vmin + net_.buses[br.to].vmax);
+        double* pt = &s.bp[6 * static_cast<size_t>(b)];
+        pt[0] = vi; pt[1] = vj; pt[2] = 0.0; pt[3] = 0.0; pt[4] = 0.0; pt[5] = 0.0;
+        double f[4];
+        branch_flows_host(br.y, vi, vj, 0.0, 0.0, f);
+        const double vals[8] = {f[0], f[1], f[2], f[3], vi * vi, 0.0, vj * vj, 0.0};
+        const int base = 2 * ng + 8 * b;
+        for (int k = 0; k < 8; ++k) s.x[base + k] = s.xbar[base + k] = vals[k];
+        if (br.limited()) {
+            const double rt = cfg_.limit_tighten * br.rate;
+            pt[4] = sclamp(-(f[0] * f[0] + f[1] * f[1]), -rt * rt, 0.0);
+            pt[5] = sclamp(-(f[2] * f[2] + f[3] * f[3]), -rt * rt, 0.0);
+        }
+    }
+    upload_state(s);
+}
+
+void Session::upload_state(const HostState& s) {
+    const size_t nl = static_cast<size_t>(dn_.nl);
+    auto put = [&](double* dst, const std::vector<double>& v) {
+        if (!v.empty())
+            check(cudaMemcpyAsync(dst, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                  stream_),
+                  "upload_state");
+    };
+    put(ds_.x, s.x); put(ds_.xbar, s.xbar); put(ds_.z, s.z); put(ds_.y, s.y);
+    put(ds_.lambda, s.lambda); put(ds_.rho, s.rho);
+    put(ds_.bus_w, s.bus_w); put(ds_.bus_theta, s.bus_theta);
+    if (!s.bp.empty()) {  // branch-major (host) -> component-major (device)
+        std::vector<double> t(6 * nl);
+        for (size_t b = 0; b < nl; ++b)
+            for (int k = 0; k < 6; ++k) t[k * nl + b] = s.bp[6 * b + k];
+        check(cudaMemcpyAsync(ds_.bp, t.data(), t.size() * sizeof(double), cudaMemcpyHostToDevice,
+                              stream_),
+              "upload bp");
+        check(cudaStreamSynchronize(stream_), "sync");
+    }
+    put(ds_.lt_ij, s.lt_ij); put(ds_.lt_ji, s.lt_ji); put(ds_.rho_t, s.rho_t);
+    beta_ = s.beta;
+    check(cudaStreamSynchronize(stream_), "sync");
+}
+
+void Session::download_state(HostState& s) const {
+    const int m = dn_.m, nb = dn_.nb;
+    const size_t nl = static_cast<size_t>(dn_.nl);
+    auto get = [&](std::vector<double>& v, const double* src, size_t n) {
+        v.resize(n);
+        if (n) check(cudaMemcpyAsync(v.data(), src, n * sizeof(double), cudaMemcpyDeviceToHost, stream_),
+                     "download_state");
+    };
+    get(s.x, ds_.x, m); get(s.xbar, ds_.xbar, m); get(s.z, ds_.z, m); get(s.y, ds_.y, m);
+    get(s.lambda, ds_.lambda, m); get(s.rho, ds_.rho, m);
+    get(s.bus_w, ds_.bus_w, nb); get(s.bus_theta, ds_.bus_theta, nb);
+    std::vector<double> t;
+    get(t, ds_.bp, 6 * nl);
+    get(s.lt_ij, ds_.lt_ij, nl); get(s.lt_ji, ds_.lt_ji, nl); get(s.rho_t, ds_.rho_t, nl);
+    check(cudaStreamSynchronize(stream_), "sync");
+    s.bp.resize(6 * nl);
+    for (size_t b = 0; b < nl; ++b)
+        for (int k = 0; k < 6; ++k) s.bp[6 * b + k] = t[k * nl + b];
+    s.beta = beta_;
+}
+
+void Session::download_solution_inputs(std::vector<double>& gen_rows, std::vector<double>& w,
+                                       std::vector<double>& th) const {
+    gen_rows.resize(2 * static_cast<size_t>(dn_.ng));
+    w.resize(dn_.nb);
+    th.resize(dn_.nb);
+    if (!gen_rows.empty())
+        check(cudaMemcpyAsync(gen_rows.data(), ds_.x, gen_rows.size() * sizeof(double),
+                              cudaMemcpyDeviceToHost, stream_), "D2H");
+    if (dn_.nb) {
+        check(cudaMemcpyAsync(w.data(), ds_.bus_w, w.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                              stream_), "D2H");
+        check(cudaMemcpyAsync(th.data(), ds_.bus_theta, th.size() * sizeof(double),
+                              cudaMemcpyDeviceToHost, stream_), "D2H");
+    }
+    check(cudaStreamSynchronize(stream_), "sync");
+}
+
+void Session::set_loads(const std::vector<double>& pd, const std::vector<double>& qd) {
+    check(cudaMemcpyAsync(dn_.b_pd, pd.data(), pd.size() * sizeof(double), cudaMemcpyHostToDevice,
+                          stream_), "set_loads");
+    check(cudaMemcpyAsync(dn_.b_qd, qd.data(), qd.size() * sizeof(double), cudaMemcpyHostToDevice,
+                          stream_), "set_loads");
+    check(cudaStreamSynchronize(stream_), "sync");
+}
+
+void Session::set_gen_p_bounds(const std::vector<double>& pmin, const std::vector<double>& pmax) {
+    check(cudaMemcpyAsync(dn_.g_pmin, pmin.data(), pmin.size() * sizeof(double),
+                          cudaMemcpyHostToDevice, stream_), "set_gen_p_bounds");
+    check(cudaMemcpyAsync(dn_.g_pmax, pmax.data(), pmax.size() * sizeof(double),
+                          cudaMemcpyHostToDevice, stream_), "set_gen_p_bounds");
+    check(cudaStreamSynchronize(stream_), "sync");
+}
+
+void Session::clamp_gen_p() {
+    launch_clamp_gen_p(dn_, ds_, stream_);
+    check(cudaGetLastError(), "clamp_gen_p");
+}
+
+BranchCfg branch_cfg(const SolverConfig& c) {
+    BranchCfg b = c.tron;
+    b.limit_tighten = c.limit_tighten;
+    return b;
+}
+
+long Session::run_phase(int phase, double z_inf, double prev_z_inf) {
+    long ret = 0;
+    launch_reset_scalars(sc_, stream_);
+    switch (phase) {
+        case 0: launch_generators(dn_, ds_, stream_); break;
+        case 1: launch_branches(dn_, ds_, branch_cfg(cfg_), sc_, stream_); break;
+        case 2: launch_buses(dn_, ds_, sc_, stream_); break;
+        case 3: launch_z_only(dn_, ds_, beta_, stream_); break;
+        case 4: launch_y_only(dn_, ds_, stream_); break;
+        case 5:
+            launch_outer(dn_, ds_, beta_, cfg_.lambda_min, cfg_.lambda_max, stream_);
+            // beta schedule (kernels.cpp:436-437)
+            if (prev_z_inf >= 0.0 && z_inf > cfg_.beta_shrink_trigger * prev_z_inf)
+                beta_ = smin(beta_ * cfg_.beta_growth, cfg_.beta_max);
+            break;
+        default: throw std::invalid_argument("unknown phase");
+    }
+    check(cudaGetLastError(), "phase launch");
+    check(cudaMemcpyAsync(sc_host_, sc_, sizeof(DevScalars), cudaMemcpyDeviceToHost, stream_), "D2H");
+    check(cudaStreamSynchronize(stream_), "phase sync");
+    if (phase == 1) ret = static_cast<long>(sc_host_->failures);
+    if (phase == 2) ret = sc_host_->singular_bus == INT32_MAX ? -1 : sc_host_->singular_bus;
+    return ret;
+}
+
+int Session::iterate(double out[4], PhaseTimes* times) {
+    launch_reset_scalars(sc_, stream_);
+    cudaEventRecord(ev_[0], stream_);
+    launch_generators(dn_, ds_, stream_);
+    cudaEventRecord(ev_[1], stream_);
+    launch_branches(dn_, ds_, branch_cfg(cfg_), sc_, stream_);
+    cudaEventRecord(ev_[2], stream_);
+    launch_buses(dn_, ds_, sc_, stream_);
+    cudaEventRecord(ev_[3], stream_);
+    launch_zy(dn_, ds_, beta_, sc_, stream_);
+    cudaEventRecord(ev_[4], stream_);
+    check(cudaGetLastError(), "iteration launch");
+    check(cudaMemcpyAsync(sc_host_, sc_, sizeof(DevScalars), cudaMemcpyDeviceToHost, stream_), "D2H");
+    check(cudaStreamSynchronize(stream_), "iteration sync");
+    float ms[4] = {0, 0, 0, 0};
+    for (int k = 0; k < 4; ++k) {
+        cudaEventElapsedTime(&ms[k], ev_[k], ev_[k + 1]);
+        clocks_[k].ms += ms[k];
+        clocks_[k].launches += 1;
+    }
+    if (times) {
+        times->x_s += (ms[0] + ms[1]) * 1e-3;
+        times->xbar_s += ms[2] * 1e-3;
+        times->z_s += ms[3] * 1e-3;  // z and y are one fused kernel
+    }
+    const DevScalars& h = *sc_host_;
+    if (h.singular_bus != INT32_MAX) {
+        const int i = h.singular_bus;
+        const int id = net_.buses[i].id;
+        throw SingularBusError(id, "isolated bus " + std::to_string(id) + ": singular balance system");
+    }
+    out[0] = from_bits(h.primal_inf);
+    out[1] = from_bits(h.dual_inf);
+    out[2] = from_bits(h.z_inf);
+    out[3] = from_bits(h.z_drift);
+    return static_cast<int>(h.failures);
+}
+
+void Session::outer_update() {
+    launch_outer(dn_, ds_, beta_, cfg_.lambda_min, cfg_.lambda_max, stream_);
+    check(cudaGetLastError(), "outer launch");
+}
+
+double Session::rho_max() {
+    launch_rowmax(ds_.rho, dn_.m, red_, stream_);
+    unsigned long long bits = 0;
+    check(cudaMemcpyAsync(&bits, red_, sizeof bits, cudaMemcpyDeviceToHost, stream_), "D2H");
+    check(cudaStreamSynchronize(stream_), "sync");
+    return from_bits(bits);
+}
+
+long long Session::tron_iterations() const {
+    DevScalars h;
+    check(cudaMemcpy(&h, sc_, sizeof h, cudaMemcpyDeviceToHost), "D2H");
+    return static_cast<long long>(h.tron_iters);
+}
+
+long long Session::sincos_calls() const {
+    DevScalars h;
+    check(cudaMemcpy(&h, sc_, sizeof h, cudaMemcpyDeviceToHost), "D2H");
+    return static_cast<long long>(h.sincos);
+}
+
+void Session::sync() const { check(cudaStreamSynchronize(stream_), "sync"); }
+
+}  // namespace ga

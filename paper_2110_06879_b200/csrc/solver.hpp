@@ -1,0 +1,201 @@
+// solver.hpp — host driver of the device-resident two-level ADMM
+// (Algorithm 1; reference proj/src/driver.{hpp,cpp}) and warm-start
+// tracking (proj/src/tracking.{hpp,cpp}).
+//
+// A Session owns one copy of the network and the full AdmmState in HBM on
+// one CUDA device plus a private stream; every inner iteration is four
+// kernel phases on that stream followed by one 56-byte D2H of the reduced
+// norms (the only host<->device traffic of the loop).  The state never
+// leaves the device between iterations, outer iterations or tracking
+// periods.
+#ifndef GA_SOLVER_HPP
+#define GA_SOLVER_HPP
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "device.hpp"
+#include "network.hpp"
+
+namespace ga {
+
+struct SolverConfig {  // proj/src/driver.hpp:15-40
+    double rho_pq = 10.0;
+    double rho_va = 1000.0;
+    double beta0 = 1e3;
+    double beta_growth = 10.0;
+    double beta_shrink_trigger = 0.25;
+    double beta_max = 1e12;
+    double eps = 1e-4;
+    double inner_tol = 0.0;
+    int max_outer = 20;
+    int max_inner = 1000;
+    double lambda_min = -1e12;
+    double lambda_max = 1e12;
+    double divergence_threshold = 1e8;
+    double limit_tighten = 0.99;
+    double warm_beta_cap = 1e6;
+    BranchCfg tron;  // gtol, max_iterations, cg_tol, max_cg, delta_floor
+    int workers = 1;  // accepted for API compatibility; unused on the GPU
+    int device = 0;
+
+    double effective_inner_tol(int m) const;
+};
+
+enum class SolveStatus { Converged = 0, IterationLimit = 1, Diverged = 2 };
+
+struct IterationRecord {
+    int outer = 0, inner = 0;
+    double primal_res = 0, dual_res = 0, z_norm = 0, elapsed_s = 0;
+};
+
+struct Solution {
+    std::vector<double> pg, qg, vm, va;
+    std::vector<double> flows;  // 4 per branch: pij, qij, pji, qji
+};
+
+struct QualityMetrics {
+    double balance_inf = 0, limit_violation = 0, bound_violation = 0, c_inf = 0, objective = 0;
+};
+
+struct PhaseTimes {
+    double x_s = 0, xbar_s = 0, z_s = 0, y_s = 0;
+};
+
+struct SolveReport {
+    SolveStatus status = SolveStatus::IterationLimit;
+    std::vector<IterationRecord> series;
+    int outer_iterations = 0;
+    int inner_iterations = 0;
+    int branch_solve_failures = 0;
+    PhaseTimes phase_times;
+    Solution solution;
+    QualityMetrics quality;
+    std::string diagnostic;
+};
+
+class SingularBusError : public std::runtime_error {
+public:
+    SingularBusError(int bus_id, const std::string& w) : std::runtime_error(w), bus(bus_id) {}
+    int bus;
+};
+
+class CudaError : public std::runtime_error {
+public:
+    explicit CudaError(const std::string& w) : std::runtime_error(w) {}
+};
+
+// Host copy of one AdmmState (proj/src/decomp.hpp:64-78); bp is 6 per
+// branch, branch-major as in the reference.
+struct HostState {
+    std::vector<double> x, xbar, z, y, lambda, rho, bus_w, bus_theta, bp, lt_ij, lt_ji, rho_t;
+    double beta = 0.0;
+};
+
+struct KernelClock {
+    double ms = 0.0;
+    long long launches = 0;
+};
+
+class Session {
+public:
+    Session(const Network& net, const SolverConfig& cfg);
+    ~Session();
+    Session(const Session&) = delete;
+    Session& operator=(const Session&) = delete;
+
+    const Network& network() const { return net_; }
+    const SolverConfig& config() const { return cfg_; }
+    int m() const { return dn_.m; }
+
+    void cold_start();                      // driver.cpp:26-63 (host) -> upload
+    void upload_state(const HostState& s);  // any empty vector is skipped
+    void download_state(HostState& s) const;
+    double beta() const { return beta_; }
+    void set_beta(double b) { beta_ = b; }
+
+    // Tracking: per-period loads and generator p-bounds (tracking.cpp:14-26,50-63).
+    void set_loads(const std::vector<double>& pd, const std::vector<double>& qd);
+    void set_gen_p_bounds(const std::vector<double>& pmin, const std::vector<double>& pmax);
+    void clamp_gen_p();
+
+    // One phase (phase-replay API).  Returns failures / singular bus / 0.
+    long run_phase(int phase, double z_inf, double prev_z_inf);
+
+    // One fused inner iteration: gen, branch, bus, z/y/norms, then one D2H of
+    // the scalars.  Fills out[0..3] = primal_inf, dual_inf (raw, before
+    // rho_max), z_inf, z_drift; returns branch failures; throws
+    // SingularBusError.
+    int iterate(double out[4], PhaseTimes* times);
+    void outer_update();                       // lambda clamp on the device
+    double rho_max();                          // max over rows, device reduction
+
+    KernelClock kernel_clock(int cls) const { return clocks_[cls]; }
+    long long tron_iterations() const;
+    long long sincos_calls() const;
+    void sync() const;
+
+    // Solution extraction inputs: x gen rows, bus_w, bus_theta.
+    void download_solution_inputs(std::vector<double>& gen_rows, std::vector<double>& w,
+                                  std::vector<double>& th) const;
+
+private:
+    void upload_network();
+    void free_all();
+    Network net_;
+    SolverConfig cfg_;
+    DevNet dn_;
+    DevState ds_;
+    DevScalars* sc_ = nullptr;       // device
+    DevScalars* sc_host_ = nullptr;  // pinned mirror
+    unsigned long long* red_ = nullptr;
+    double beta_ = 0.0;
+    cudaStream_t stream_ = nullptr;
+    cudaEvent_t ev_[5] = {};
+    KernelClock clocks_[4];
+    std::vector<void*> allocs_;
+};
+
+SolveReport solve(Session& s, const SolverConfig& cfg, bool warm);
+
+Solution extract_solution(const Network& net, const std::vector<double>& gen_rows,
+                          const std::vector<double>& bus_w, const std::vector<double>& bus_theta);
+QualityMetrics evaluate_solution(const Network& net, const Solution& sol);
+
+// ---- tracking (tracking.hpp) --------------------------------------------
+class RampError : public std::runtime_error {
+public:
+    RampError(int period, int gen, const std::string& w)
+        : std::runtime_error(w), period(period), generator(gen) {}
+    int period, generator;
+};
+
+struct TrackingScenario {
+    std::vector<double> multipliers;
+    std::vector<std::vector<double>> per_bus;
+    double ramp_fraction = 0.02;
+    int periods() const { return static_cast<int>(multipliers.size()); }
+};
+
+struct PeriodReport {
+    int period = 0;
+    SolveReport report;
+    double time_s = 0.0;
+};
+
+std::vector<PeriodReport> run_tracking(const Network& net, const SolverConfig& cfg,
+                                       const TrackingScenario& sc);
+TrackingScenario load_profile_csv(const std::string& path, const Network& net);
+
+// ---- outputs (outputs.hpp) ----------------------------------------------
+double report_gap(double objective, double reference);
+void write_solution_json(const std::string& path, const Network& net, const SolveReport& r,
+                         double ref_objective);
+void write_convergence_csv(const std::string& path, const std::vector<IterationRecord>& s);
+void write_periods_csv(const std::string& path, const std::vector<PeriodReport>& p,
+                       const std::vector<double>& refs);
+
+}  // namespace ga
+
+#endif

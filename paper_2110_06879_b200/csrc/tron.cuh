@@ -1,0 +1,422 @@
+// tron.cuh — batched trust-region Newton (TRON) for tiny dense box-constrained
+// NLPs, one solve per CUDA thread, all arrays register-resident.
+//
+// Algorithm: proj/src/tron.cpp (reference).  This is a fresh sm_100a
+// formulation, not a translation of the reference's data structures:
+//  * the dimension N (4 or 6 for branches) is a template parameter, so every
+//    vector/matrix index is a compile-time constant and nothing touches local
+//    memory;
+//  * the reduced ("free") subspace of subspace_cg is not gathered into a
+//    packed nf x nf copy (tron.cpp:154-159) — it is a bitmask over the full
+//    N-space, and every reduced-space loop is a predicated full-space loop
+//    that visits the free indices in ascending order, which is exactly the
+//    packed order, so every reduction happens in the reference's order;
+//  * the solve is a resumable state machine (TronState + tron_step) so a
+//    persistent warp can interleave many solves per lane (branch.cu).
+//
+// Bit-exactness rules: compiled with -fmad=false, IEEE
+// div/sqrt; every sum is sequential left-to-right starting at +0.0 as in
+// tron.cpp:16-20,35-43,62-89; std::min/max/clamp via ga_math.h.
+#ifndef GA_TRON_CUH
+#define GA_TRON_CUH
+
+#include "ga_math.h"
+
+namespace ga {
+
+struct TronParams {           // proj/src/tron.hpp:24-30
+    double gtol = 1e-6;
+    int max_iterations = 200;
+    double cg_tol = 0.1;
+    int max_cg = 32;
+    double delta_floor = 1e-3;
+};
+
+constexpr double kTronMu0 = 0.01;     // tron.cpp:10
+constexpr double kTronEta = 1e-4;     // tron.cpp:11
+constexpr double kTronDeltaMax = 1e10; // tron.cpp:12
+
+enum TronStatusCode : int { kTronConverged = 0, kTronIterationLimit = 1, kTronNumericalError = 2 };
+
+// ---- sequential reductions over N (tron.cpp:16-51) ------------------------
+
+template <int N>
+GA_FN double vdot(const double* a, const double* b) {
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) s += a[i] * b[i];
+    return s;
+}
+
+template <int N>
+GA_FN double vnorm2(const double* a) { return sqrt(vdot<N>(a, a)); }
+
+// q(s) = g's + sum_i 0.5*s_i*(H s)_i  (tron.cpp:35-43)
+template <int N>
+GA_FN double model(const double* g, const double* h, const double* s) {
+    double q = vdot<N>(g, s);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        double hs = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) hs += h[i * N + j] * s[j];
+        q += 0.5 * s[i] * hs;
+    }
+    return q;
+}
+
+// Reduced-space dot over the free mask (ascending = packed order).
+template <int N>
+GA_FN double mdot(unsigned fm, const double* a, const double* b) {
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+        if (fm >> i & 1u) s += a[i] * b[i];
+    return s;
+}
+
+// Cholesky of the free principal submatrix (tron.cpp:53-67): reads the lower
+// triangle h[i][j], i > j, as the reference's hf does.
+template <int N>
+GA_FN bool mcholesky(unsigned fm, const double* h, double* L) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        if (!(fm >> j & 1u)) continue;
+        double d = h[j * N + j];
+#pragma unroll
+        for (int k = 0; k < j; ++k)
+            if (fm >> k & 1u) d -= L[j * N + k] * L[j * N + k];
+        if (d <= 0.0 || !sfinite(d)) return false;
+        L[j * N + j] = sqrt(d);
+#pragma unroll
+        for (int i = j + 1; i < N; ++i) {
+            if (!(fm >> i & 1u)) continue;
+            double v = h[i * N + j];
+#pragma unroll
+            for (int k = 0; k < j; ++k)
+                if (fm >> k & 1u) v -= L[i * N + k] * L[j * N + k];
+            L[i * N + j] = v / L[j * N + j];
+        }
+    }
+    return true;
+}
+
+// (L L')^{-1} b on the free set (tron.cpp:69-80).
+template <int N>
+GA_FN void mchol_solve(unsigned fm, const double* L, const double* b, double* x) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        if (!(fm >> i & 1u)) continue;
+        double v = b[i];
+#pragma unroll
+        for (int k = 0; k < i; ++k)
+            if (fm >> k & 1u) v -= L[i * N + k] * x[k];
+        x[i] = v / L[i * N + i];
+    }
+#pragma unroll
+    for (int i = N - 1; i >= 0; --i) {
+        if (!(fm >> i & 1u)) continue;
+        double v = x[i];
+#pragma unroll
+        for (int k = i + 1; k < N; ++k)
+            if (fm >> k & 1u) v -= L[k * N + i] * x[k];
+        x[i] = v / L[i * N + i];
+    }
+}
+
+// Largest tau >= 0 with ||s + tau p|| = delta (tron.cpp:83-90), full space.
+template <int N>
+GA_FN double boundary_tau(const double* s, const double* p, double delta) {
+    const double pp = vdot<N>(p, p);
+    if (pp <= 0.0) return 0.0;
+    const double sp = vdot<N>(s, p);
+    const double ss = vdot<N>(s, s);
+    const double disc = smax(0.0, sp * sp + pp * (delta * delta - ss));
+    return (-sp + sqrt(disc)) / pp;
+}
+
+// Cauchy point (tron.cpp:101-137).
+template <int N>
+GA_FN void cauchy_point(const double* x, const double* g, const double* h,
+                        const double* l, const double* u, double delta, double* s) {
+    const double gnorm = vnorm2<N>(g);
+    if (gnorm == 0.0) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) s[i] = 0.0;
+        return;
+    }
+    auto step_at = [&](double alpha, double* out) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) out[i] = sclamp(x[i] - alpha * g[i], l[i], u[i]) - x[i];
+    };
+    auto ok = [&](const double* st) {
+        if (!(vnorm2<N>(st) <= delta)) return false;
+        return model<N>(g, h, st) <= kTronMu0 * vdot<N>(g, st);
+    };
+    double alpha = smin(1.0, delta / gnorm);
+    step_at(alpha, s);
+    if (ok(s)) {
+        double trial[N];
+        for (int it = 0; it < 20; ++it) {
+            const double next = alpha * 2.0;
+            step_at(next, trial);
+            if (!ok(trial)) break;
+            alpha = next;
+#pragma unroll
+            for (int i = 0; i < N; ++i) s[i] = trial[i];
+        }
+        return;
+    }
+    for (int it = 0; it < 40; ++it) {
+        alpha *= 0.5;
+        step_at(alpha, s);
+        if (ok(s)) return;
+    }
+}
+
+// Preconditioned Steihaug CG on the free subspace at x + s
+// (tron.cpp:141-224).  d receives the full-space correction.
+template <int N>
+GA_FN void subspace_cg(const double* x, const double* g, const double* h,
+                       const double* l, const double* u, double delta,
+                       const TronParams& cfg, const double* s, double* d) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) d[i] = 0.0;
+    unsigned fm = 0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const double xi = x[i] + s[i];
+        if (xi > l[i] && xi < u[i]) fm |= 1u << i;
+    }
+    if (fm == 0) return;
+
+    double rf[N], L[N * N], zk[N], pk[N], dk[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {  // rf = -(g + H s) on the free set
+        double hs = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) hs += h[i * N + j] * s[j];
+        rf[i] = -(g[i] + hs);
+        dk[i] = 0.0;
+    }
+    const bool have_prec = mcholesky<N>(fm, h, L);
+    if (have_prec) mchol_solve<N>(fm, L, rf, zk);
+    else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) zk[i] = rf[i];
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) pk[i] = zk[i];
+    double rz = mdot<N>(fm, rf, zk);
+    const double r0 = sqrt(mdot<N>(fm, rf, rf));
+    if (r0 == 0.0) return;
+
+    for (int it = 0; it < cfg.max_cg; ++it) {
+        double hpk[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            double v = 0.0;
+#pragma unroll
+            for (int j = 0; j < N; ++j)
+                if (fm >> j & 1u) v += h[i * N + j] * pk[j];
+            hpk[i] = v;
+        }
+        const double curv = mdot<N>(fm, pk, hpk);
+        double pfull[N], sd[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            const bool fr = fm >> i & 1u;
+            pfull[i] = fr ? pk[i] : 0.0;
+            sd[i] = s[i] + (fr ? dk[i] : 0.0);
+        }
+        if (curv <= 0.0) {  // negative curvature: to the boundary
+            const double tau = boundary_tau<N>(sd, pfull, delta);
+#pragma unroll
+            for (int i = 0; i < N; ++i)
+                if (fm >> i & 1u) dk[i] += tau * pk[i];
+            break;
+        }
+        const double alpha = rz / curv;
+        double dnext[N], snext[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            const bool fr = fm >> i & 1u;
+            dnext[i] = dk[i] + alpha * pk[i];
+            snext[i] = s[i] + (fr ? dnext[i] : 0.0);
+        }
+        if (vnorm2<N>(snext) >= delta) {
+            const double tau = boundary_tau<N>(sd, pfull, delta);
+#pragma unroll
+            for (int i = 0; i < N; ++i)
+                if (fm >> i & 1u) dk[i] += tau * pk[i];
+            break;
+        }
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+            if (fm >> i & 1u) {
+                dk[i] = dnext[i];
+                rf[i] -= alpha * hpk[i];
+            }
+        if (sqrt(mdot<N>(fm, rf, rf)) <= cfg.cg_tol * r0) break;
+        double znext[N];
+        if (have_prec) mchol_solve<N>(fm, L, rf, znext);
+        else {
+#pragma unroll
+            for (int i = 0; i < N; ++i) znext[i] = rf[i];
+        }
+        const double rznext = mdot<N>(fm, rf, znext);
+        const double betak = rznext / rz;
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+            if (fm >> i & 1u) pk[i] = znext[i] + betak * pk[i];
+        rz = rznext;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) d[i] = (fm >> i & 1u) ? dk[i] : 0.0;
+}
+
+// Projected-gradient inf-norm (tron.cpp:251-257 / 320-326); NaN entries are
+// skipped exactly like std::max(pgnorm, std::abs(gi)).
+template <int N>
+GA_FN double proj_grad_norm(const double* x, const double* g, const double* l,
+                            const double* u) {
+    double pg = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        double gi = g[i];
+        if (x[i] <= l[i]) gi = smin(gi, 0.0);
+        else if (x[i] >= u[i]) gi = smax(gi, 0.0);
+        pg = smax(pg, fabs(gi));
+    }
+    return pg;
+}
+
+// Resumable solve_one (tron.cpp:228-332).
+template <int N>
+struct TronState {
+    double x[N];
+    double f;
+    double delta;
+    int iter;
+};
+
+// Starts a solve: clip x into the box and evaluate f (tron.cpp:235-240).
+// Returns false (NumericalError, iterations 0) when f is not finite.
+template <int N, class P>
+GA_FN bool tron_begin(const P& prob, TronState<N>& st) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) st.x[i] = sclamp(st.x[i], prob.lo(i), prob.hi(i));
+    st.f = prob.value(st.x);
+    st.delta = 0.0;
+    st.iter = 0;
+    return sfinite(st.f);
+}
+
+enum TronStep : int { kStepContinue = 0, kStepConverged = 1, kStepError = 2, kStepExhausted = 3 };
+
+// One trust-region iteration (tron.cpp:243-317).  kStepExhausted means the
+// loop ended by the iteration cap or the delta < 1e-14 break, after which
+// tron_finish must be called.  *evals counts value/gradient calls.
+template <int N, class P>
+GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg) {
+    double l[N], u[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) { l[i] = prob.lo(i); u[i] = prob.hi(i); }
+    double g[N];
+    prob.gradient(st.x, g);
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+        if (!sfinite(g[i])) return kStepError;
+    if (proj_grad_norm<N>(st.x, g, l, u) <= cfg.gtol) return kStepConverged;
+    double h[N * N];
+    prob.hessian(st.x, h);
+#pragma unroll
+    for (int i = 0; i < N * N; ++i)
+        if (!sfinite(h[i])) return kStepError;
+    if (st.iter == 0 && st.delta == 0.0) st.delta = smax(vnorm2<N>(g), cfg.delta_floor);
+
+    double s[N], d[N];
+    cauchy_point<N>(st.x, g, h, l, u, st.delta, s);
+    subspace_cg<N>(st.x, g, h, l, u, st.delta, cfg, s, d);
+
+    const double qc = model<N>(g, h, s);
+    double stp[N];
+    double beta = 1.0;
+    bool used_d = false;
+    for (int ls = 0; ls < 20; ++ls) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) stp[i] = sclamp(st.x[i] + s[i] + beta * d[i], l[i], u[i]) - st.x[i];
+        if (model<N>(g, h, stp) <= qc) { used_d = true; break; }
+        beta *= 0.5;
+    }
+    if (!used_d) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) stp[i] = s[i];
+    }
+    const double q = model<N>(g, h, stp);
+    double xt[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) xt[i] = sclamp(st.x[i] + stp[i], l[i], u[i]);
+    const double ft = prob.value(xt);
+    if (!sfinite(ft)) return kStepError;
+    const double ared = st.f - ft;
+    const double pred = -q;
+    const double ratio = pred > 0.0 ? ared / pred : (ared > 0.0 ? 1.0 : -1.0);
+    const double snorm = vnorm2<N>(stp);
+    if (ratio < 0.25) st.delta = 0.25 * smax(snorm, 1e-12);
+    else if (ratio > 0.75 && snorm >= 0.9 * st.delta) st.delta = smin(2.0 * st.delta, kTronDeltaMax);
+    if (ared > 0.0 && ratio > kTronEta) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) st.x[i] = xt[i];
+        st.f = ft;
+    }
+    ++st.iter;
+    if (st.delta < 1e-14 || st.iter >= cfg.max_iterations) return kStepExhausted;
+    return kStepContinue;
+}
+
+// Post-loop status (tron.cpp:320-330): gradient at x (no finiteness check),
+// projected-gradient test.
+template <int N, class P>
+GA_FN int tron_finish(const P& prob, const TronState<N>& st, const TronParams& cfg) {
+    double l[N], u[N], g[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) { l[i] = prob.lo(i); u[i] = prob.hi(i); }
+    prob.gradient(st.x, g);
+    return proj_grad_norm<N>(st.x, g, l, u) <= cfg.gtol ? kTronConverged : kTronIterationLimit;
+}
+
+// Whole solve (used by the QP test kernel and the simple branch path).
+// Returns the status; *iterations follows TronResult::iterations semantics.
+template <int N, class P>
+GA_FN int tron_solve(const P& prob, double* x, const TronParams& cfg, int* iterations) {
+    TronState<N> st;
+#pragma unroll
+    for (int i = 0; i < N; ++i) st.x[i] = x[i];
+    int status;
+    if (!tron_begin<N>(prob, st)) {
+        *iterations = 0;
+        status = kTronNumericalError;
+    } else if (cfg.max_iterations <= 0) {
+        *iterations = cfg.max_iterations;
+        status = tron_finish<N>(prob, st, cfg);
+    } else {
+        for (;;) {
+            const int iter_before = st.iter;
+            const int r = tron_step<N>(prob, st, cfg);
+            if (r == kStepContinue) continue;
+            if (r == kStepConverged) { *iterations = iter_before; status = kTronConverged; break; }
+            if (r == kStepError) { *iterations = iter_before; status = kTronNumericalError; break; }
+            *iterations = cfg.max_iterations;
+            status = tron_finish<N>(prob, st, cfg);
+            break;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = st.x[i];
+    return status;
+}
+
+}  // namespace ga
+
+#endif

@@ -54,6 +54,22 @@ typedef enum gridadmm_phase {
 /* Number of m rows of the coupling layout (2G + 8L). */
 int gridadmm_network_num_rows(const gridadmm_network* net);
 
+/* Parsed network in flat arrays (host only, no device needed), for checking
+ * the parser against the reference's (proj/src/netdata.cpp:124-237):
+ * bus 6 per bus (pd, qd, gs, bs, vmin, vmax) + external ids; gen 8 per gen
+ * (bus, pmin, pmax, qmin, qmax, c2, c1, c0); branch ends 2 per branch and 14
+ * doubles (r, x, b, tap, shift, rate, gii, bii, gij, bij, gji, bji, gjj, bjj).
+ * Any pointer may be NULL. */
+gridadmm_status gridadmm_network_export(const gridadmm_network* net, double* bus,
+                                        int* bus_id, double* gen, int* ends,
+                                        double* branch, int* ref_bus);
+
+/* Bus-owned row lists of the coupling layout (proj/src/decomp.cpp:7-31):
+ * counts[6*i + k] = sizes of (gen_p, gen_q, flow_p, flow_q, w, theta) of bus
+ * i, rows = the lists concatenated per bus in that group order (length m). */
+gridadmm_status gridadmm_network_layout(const gridadmm_network* net, int* counts,
+                                        int* rows);
+
 /* Creates a device-resident session for (net, cfg) on the configured device
  * and loads the cold-start state (proj/src/driver.cpp:26-63). */
 gridadmm_status gridadmm_session_new(const gridadmm_network* net,

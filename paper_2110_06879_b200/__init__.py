@@ -76,6 +76,8 @@ SYMBOLS = {
 }
 EXT_SYMBOLS = {
     "gridadmm_network_num_rows": (_I, [_P]),
+    "gridadmm_network_export": (_I, [_P, _DP, _IP, _DP, _IP, _DP, _IP]),
+    "gridadmm_network_layout": (_I, [_P, _IP, _IP]),
     "gridadmm_session_new": (_I, [_P, _P, ctypes.POINTER(_P)]),
     "gridadmm_session_free": (None, [_P]),
     "gridadmm_session_get_state": (_I, [_P, ctypes.POINTER(StateView)]),
@@ -169,6 +171,26 @@ class Network:
     @property
     def num_rows(self) -> int:
         return lib().gridadmm_network_num_rows(self._h)
+
+    def export(self):
+        nb, ng, nl = self.num_buses, self.num_generators, self.num_branches
+        bus = np.zeros(6 * nb)
+        ids = np.zeros(nb, dtype=np.int32)
+        gen = np.zeros(8 * ng)
+        ends = np.zeros(2 * nl, dtype=np.int32)
+        br = np.zeros(14 * nl)
+        ref = ctypes.c_int()
+        _check(lib().gridadmm_network_export(self._h, _dp(bus), ids.ctypes.data_as(_IP), _dp(gen),
+                                             ends.ctypes.data_as(_IP), _dp(br), ctypes.byref(ref)))
+        return {"bus": bus.reshape(-1, 6), "bus_id": ids, "gen": gen.reshape(-1, 8),
+                "ends": ends.reshape(-1, 2), "branch": br.reshape(-1, 14), "ref_bus": ref.value}
+
+    def layout(self):
+        counts = np.zeros(6 * self.num_buses, dtype=np.int32)
+        rows = np.zeros(max(self.num_rows, 1), dtype=np.int32)
+        _check(lib().gridadmm_network_layout(self._h, counts.ctypes.data_as(_IP),
+                                             rows.ctypes.data_as(_IP)))
+        return counts.reshape(-1, 6), rows[: self.num_rows]
 
     def close(self):
         if getattr(self, "_h", None):

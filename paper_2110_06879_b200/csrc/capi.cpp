@@ -147,6 +147,60 @@ int gridadmm_network_num_generators(const gridadmm_network* n) { return n ? n->n
 int gridadmm_network_num_branches(const gridadmm_network* n) { return n ? n->net.nl() : 0; }
 int gridadmm_network_num_rows(const gridadmm_network* n) { return n ? n->net.m() : 0; }
 
+gridadmm_status gridadmm_network_export(const gridadmm_network* n, double* bus, int* bus_id,
+                                        double* gen, int* ends, double* branch, int* ref_bus) {
+    if (!n) return fail(GRIDADMM_ERR_INVALID_ARG, "null network");
+    const ga::Network& net = n->net;
+    for (int i = 0; i < net.nb(); ++i) {
+        const ga::Bus& b = net.buses[i];
+        if (bus) {
+            const double v[6] = {b.pd, b.qd, b.gs, b.bs, b.vmin, b.vmax};
+            std::memcpy(bus + 6 * i, v, sizeof v);
+        }
+        if (bus_id) bus_id[i] = b.id;
+    }
+    for (int g = 0; g < net.ng(); ++g) {
+        const ga::Gen& x = net.gens[g];
+        if (gen) {
+            const double v[8] = {double(x.bus), x.pmin, x.pmax, x.qmin, x.qmax, x.c2, x.c1, x.c0};
+            std::memcpy(gen + 8 * g, v, sizeof v);
+        }
+    }
+    for (int l = 0; l < net.nl(); ++l) {
+        const ga::Line& x = net.lines[l];
+        if (ends) {
+            ends[2 * l] = x.from;
+            ends[2 * l + 1] = x.to;
+        }
+        if (branch) {
+            const double v[6] = {x.r, x.x, x.b, x.tap, x.shift, x.rate};
+            std::memcpy(branch + 14 * l, v, sizeof v);
+            std::memcpy(branch + 14 * l + 6, x.y.c, sizeof x.y.c);
+        }
+    }
+    if (ref_bus) *ref_bus = net.ref_bus;
+    return GRIDADMM_OK;
+}
+
+gridadmm_status gridadmm_network_layout(const gridadmm_network* n, int* counts, int* rows) {
+    if (!n) return fail(GRIDADMM_ERR_INVALID_ARG, "null network");
+    const ga::BusCsr csr = ga::build_bus_csr(n->net);
+    // device CSR groups are [w, theta, gen_p, gen_q, flow_p, flow_q]; the
+    // reference's BusRows order is (gen_p, gen_q, flow_p, flow_q, w, theta)
+    static const int order[6] = {2, 3, 4, 5, 0, 1};
+    int pos = 0;
+    for (int i = 0; i < n->net.nb(); ++i) {
+        for (int k = 0; k < 6; ++k) {
+            const int g = order[k];
+            const int a = csr.grp[7 * i + g], b = csr.grp[7 * i + g + 1];
+            if (counts) counts[6 * i + k] = b - a;
+            for (int j = a; j < b; ++j)
+                if (rows) rows[pos++] = csr.rows[j];
+        }
+    }
+    return GRIDADMM_OK;
+}
+
 gridadmm_config* gridadmm_config_new(void) { return new gridadmm_config{}; }
 void gridadmm_config_free(gridadmm_config* cfg) { delete cfg; }
 

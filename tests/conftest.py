@@ -7,7 +7,7 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if REPO not in sys.path:
     sys.path.insert(0, REPO)
 
-CASES = os.path.join(REPO, "tests", "golden", "cases")
+CASES = os.path.join(REPO, "data")
 GOLDEN = os.path.join(REPO, "tests", "golden")
 
 

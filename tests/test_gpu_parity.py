@@ -137,11 +137,12 @@ def test_residual_series_first_iterations(gridadmm, oracle_mod, name, iters):
     assert_bits_equal(rec[:n, 0], series[:n, 2], f"{name} primal")
     assert_bits_equal(rec[:n, 1], series[:n, 3], f"{name} dual")
     assert_bits_equal(rec[:n, 2], series[:n, 4], f"{name} z_norm")
-    g = sess.get_state()
-    for f in FIELDS:
-        if f == "beta":
-            continue
-        assert_bits_equal(g[f], fin[f], f"{name} final {f}")
+    # the reference closes its single outer iteration with update_outer unless
+    # ||z||_inf <= eps (driver.cpp:224-238); do the same on the device
+    z_last = float(rec[-1, 2])
+    if not z_last <= d["eps"]:
+        sess.phase("outer", z_last, -1.0)
+    assert_state_equal(sess.get_state(), fin, f"{name} final")
 
 
 def test_full_solve_case9_through_c_abi(gridadmm, oracle_mod, tmp_path):

@@ -1,0 +1,348 @@
+#!/usr/bin/env python3
+"""bench.py — ADMM iterations/s of the B200-native gridadmm on an
+ACTIVSg70k-shaped grid (BASELINE.json metric, config[3]).
+
+A "step" is one inner ADMM iteration of the two-level ADMM (generator
+projection -> branch NLPs -> bus consensus -> z/y/residual norms, plus the
+host's read of the four residual norms that drive the loop control;
+proj/src/driver.cpp:155-186) over the whole grid.  The first W iterations
+from the cold start are the warm-up, the next K are timed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+* `value`: K x ranks / max-over-ranks device time of the K steps, state
+  resident in HBM, each step timed with CUDA events on the solver's stream
+  and an L2 flush (256 MiB write) between steps outside the events.
+* `e2e`: the same metric through the public C ABI with host buffers:
+  gridadmm_network_load'ed case -> gridadmm_solve (max_outer 1, max_inner
+  W+K; network + state upload, every iteration's norm readback and the
+  solution download inside the wall-clock region).
+* `roofline`: the branch-NLP kernel (dominant) against the measured FP64
+  DMUL+DADD peak (the kernel is built with -fmad=false for bit-exactness).
+* `cpu_baseline`: the reference C++ solver (oracle/_ref, compiled from the
+  reference sources with the pinned sincos) on this host's cores, timing a
+  bounded sample of the SAME iterations (its trajectory is bit-identical).
+* `--impl reference`: that reference solver alone (rank 0), same metric.
+
+Multi-GPU (torchrun, N>1): round-1 state is independent replicas, one
+70k-shaped solve per rank ("scaling": "weak"); see DESIGN.md §Multi-GPU.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+L2_FLUSH_BYTES = 256 << 20
+SHAPE = "case_ACTIVSg70k"
+# Lean FP64 op census per TRON iteration (flops whose results are consumed),
+# measured by the instrumented C restatement (oracle/gridadmm_oracle.c,
+# census build) — see DESIGN.md §Roofline.
+CENSUS_FLOPS = {4: 1900.0, 6: 3600.0}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--shape", default=SHAPE)
+    ap.add_argument("--seed", type=int, default=2110)
+    ap.add_argument("--preset", default="case_ACTIVSg70k")
+    ap.add_argument("--cpu-steps", type=int, default=6, help="timed iterations of the CPU sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl")
+            self.dist = dist
+            self.torch = torch
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def case_file(shape: str, seed: int, d: Dist) -> str:
+    from paper_2110_06879_b200 import synth
+    directory = os.path.join("/tmp", "gridadmm_cases")
+    path = os.path.join(directory, f"{shape}_synth_s{seed}.m")
+    if d.rank == 0:
+        synth.ensure_case(shape, directory, seed=seed)
+    d.barrier()
+    while not os.path.exists(path):  # ranks on the same host share /tmp
+        time.sleep(0.2)
+    return path
+
+
+def cfg_kwargs(args, max_inner):
+    return dict(max_outer=1, max_inner=max_inner)
+
+
+def reference_rate(path, args, iters_timed, workers):
+    """Reference C++ solver (oracle/_ref) on host cores: iterations/s over
+    iterations W..W+iters_timed-1 from the elapsed_s stamps of its own series
+    (proj/src/driver.cpp:190-191)."""
+    import oracle
+    from paper_2110_06879_b200 import Config
+    if not oracle.have_ref():
+        raise RuntimeError("oracle/_ref/libgridadmm_ref.so missing")
+    c = Config(args.preset)
+    ref = oracle.RefNet(path)
+    n = args.warmup + iters_timed
+    t0 = time.perf_counter()
+    series, info, _ = ref.solve(rho_pq=c["rho_pq"], rho_va=c["rho_va"], max_outer=1,
+                                max_inner=n, workers=workers)
+    wall = time.perf_counter() - t0
+    el = series[:, 5]
+    start = el[args.warmup - 1] if args.warmup > 0 else 0.0
+    dt = el[n - 1] - start
+    return iters_timed / dt, dt, wall, series
+
+
+def run_reference_arm(args, d: Dist):
+    if d.rank != 0:
+        return
+    path = case_file(args.shape, args.seed, d) if d.world == 1 else None
+    if path is None:
+        from paper_2110_06879_b200 import synth
+        path = synth.ensure_case(args.shape, "/tmp/gridadmm_cases", seed=args.seed)
+    workers = os.cpu_count() or 1
+    rate, dt, wall, _ = reference_rate(path, args, args.steps, workers)
+    line = {
+        "metric": "ADMM iters/sec & time-to-converge (s) on ACTIVSg70k; warm-start track s/step",
+        "impl": "reference", "value": rate, "unit": "iters/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / rate,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded tiling of MATPOWER case30/case118 to ACTIVSg70k dims)",
+        "config": {"workload": f"{args.shape}-shaped cold start, inner iterations "
+                               f"{args.warmup}..{args.warmup + args.steps - 1}",
+                   "preset": args.preset, "seed": args.seed},
+        "cpu_baseline": {"value": rate, "unit": "iters/s", "cores": workers, "kind": "reference",
+                         "sample": f"{args.steps} timed inner iterations after {args.warmup} "
+                                   f"warm-up, reference C++ solver, workers={workers}"},
+        "e2e": {"value": rate, "unit": "iters/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args, d: Dist):
+    import paper_2110_06879_b200 as ga
+    path = case_file(args.shape, args.seed, d)
+    dev = d.local
+    net = ga.Network(path)
+    cfg = ga.Config(args.preset, device=dev)
+    nb, ng, nl, m = net.num_buses, net.num_generators, net.num_branches, net.num_rows
+
+    # --- device-resident timed region -----------------------------------
+    sess = ga.Session(net, cfg)
+    sess.timed_steps(args.warmup, 0)  # warm-up iterations (untimed)
+    k0 = [sess.kernel_time(c) for c in range(4)]
+    it0 = sess.counters()
+    d.barrier()
+    with ClockSampler(dev) as clk:
+        step_ms, rec = sess.timed_steps(args.steps, L2_FLUSH_BYTES)
+    d.barrier()
+    k1 = [sess.kernel_time(c) for c in range(4)]
+    it1 = sess.counters()
+    my_ms = float(np.sum(step_ms))
+    max_ms = d.max(my_ms)
+    total_iters = d.sum(float(args.steps))
+    value = total_iters / (max_ms * 1e-3)
+
+    kern = {name: {"ms_total": k1[c][0] - k0[c][0], "launches": k1[c][1] - k0[c][1]}
+            for c, name in enumerate(["generators", "branches", "buses", "zy"])}
+    tron4 = it1[0] - it0[0]
+    tron6 = it1[1] - it0[1]
+    branch_ms = kern["branches"]["ms_total"]
+    flops = tron4 * CENSUS_FLOPS[4] + tron6 * CENSUS_FLOPS[6]
+    fp64_mul_add, fp64_fma = ga.fp64_peak(dev)
+    achieved = flops / (branch_ms * 1e-3) / 1e12 if branch_ms > 0 else 0.0
+    # HBM-bound phases: algorithmic bytes per iteration
+    hbm_bytes = {"generators": 128 * ng, "buses": 44 * m + 72 * nb, "zy": 64 * m}
+    hbm = {}
+    for name, b in hbm_bytes.items():
+        t = kern[name]["ms_total"] / max(1, kern[name]["launches"])
+        hbm[name] = {"gbs": b / (t * 1e-3) / 1e9 if t > 0 else None, "bytes": b, "ms": t}
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+
+    # --- e2e through the C ABI (host buffers) -----------------------------
+    e2e = None
+    if not args.no_e2e:
+        cfg2 = ga.Config(args.preset, device=dev, max_outer=1, max_inner=args.warmup + args.steps)
+        d.barrier()
+        t0 = time.perf_counter()
+        net2 = ga.Network(path)  # host parse -> H2D inside the solve
+        st, rep = ga.solve(net2, cfg2)
+        pg, qg = rep.dispatch()
+        vm, va = rep.voltages()
+        t_e2e = time.perf_counter() - t0
+        n_it = rep.metric("inner_iterations")
+        t_max = d.max(t_e2e)
+        h2d = (8 * (6 * ng + 10 * nl + 6 * nb) + 4 * (3 * nl + 7 * nb + m)  # network
+               + 8 * (6 * m + 2 * nb + 9 * nl))  # cold-start state
+        d2h = 56 * n_it + 8 * (2 * ng + 2 * nb)
+        e2e = {"value": d.sum(n_it) / t_max, "unit": "iters/s",
+               "h2d_bytes_per_step": h2d / n_it, "d2h_bytes_per_step": d2h / n_it,
+               "wall_s": t_max, "iterations": int(n_it),
+               "note": "gridadmm_network_load + gridadmm_solve(max_outer=1) + dispatch/voltages; "
+                       "includes parse, upload, cold start, solution download"}
+
+    # --- CPU baseline (reference on host cores), rank 0 only ---------------
+    cpu = None
+    if d.rank == 0 and d.world == 1 and not args.no_cpu_baseline:
+        workers = os.cpu_count() or 1
+        ksteps = min(args.cpu_steps, args.steps)
+        try:
+            rate, dt, wall, series = reference_rate(path, args, ksteps, workers)
+            # same trajectory: the reference's residuals must equal ours bit-for-bit
+            same = bool(np.array_equal(series[args.warmup:args.warmup + ksteps, 2:5].view(np.uint64),
+                                       rec[:ksteps, 0:3].view(np.uint64)))
+            cpu = {"value": rate, "unit": "iters/s", "cores": workers, "kind": "reference",
+                   "sample": f"inner iterations {args.warmup}..{args.warmup + ksteps - 1} of the "
+                             f"same cold start ({dt:.1f} s of {wall:.1f} s wall), reference C++ "
+                             f"solver from oracle/_ref, workers={workers}",
+                   "residuals_bit_identical_to_gpu": same}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "iters/s", "cores": workers, "kind": "reference",
+                   "sample": f"failed: {e}"}
+
+    if d.rank == 0:
+        line = {
+            "metric": "ADMM iters/sec & time-to-converge (s) on ACTIVSg70k; warm-start track s/step",
+            "value": value, "unit": "iters/s", "n_gpus": d.world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded tiling of MATPOWER case30/case118 to ACTIVSg70k dims)",
+            "config": {"workload": f"{args.shape}-shaped ({nb} buses, {ng} gens, {nl} branches, "
+                                   f"m={m}) cold start, inner iterations "
+                                   f"{args.warmup}..{args.warmup + args.steps - 1}",
+                       "preset": args.preset, "seed": args.seed,
+                       "l2": "flushed between steps (256 MiB write outside the timed events)",
+                       "parallelism": "replicas" if d.world > 1 else "single GPU"},
+            "roofline": {"bound": "fp64", "kernel": "branch_kernel (TRON branch NLPs)",
+                         "achieved": achieved, "peak": fp64_mul_add, "unit": "TFLOP/s",
+                         "frac": achieved / fp64_mul_add if fp64_mul_add else None,
+                         "traffic": None,
+                         "peak_note": "measured DMUL+DADD issue rate (kernel built -fmad=false); "
+                                      f"DFMA peak {fp64_fma:.1f} TFLOP/s",
+                         "flops_per_launch": flops / max(1, kern["branches"]["launches"]),
+                         "tron_iterations": [tron4, tron6]},
+            "roofline_hbm": {k: dict(v, peak_gbs=hbm_peak,
+                                     frac=(v["gbs"] / hbm_peak if v["gbs"] else None))
+                             for k, v in hbm.items()},
+            "kernels": kern,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": 6 * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    d = Dist()
+    try:
+        if args.impl == "reference":
+            run_reference_arm(args, d)
+        else:
+            run_b200(args, d)
+    finally:
+        d.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -100,6 +100,16 @@ gridadmm_status gridadmm_session_iterate(gridadmm_session* s, int n,
                                          double* records, int* done,
                                          int* stop);
 
+/* Benchmark form of iterate: runs exactly n inner iterations (no early
+ * stop), each bracketed by CUDA events on the session stream from the first
+ * launch through the D2H of that iteration's norms; when flush_bytes > 0 a
+ * device buffer of that size is rewritten between iterations, outside the
+ * brackets (L2 flush).  step_ms receives n device times, records 5 doubles
+ * per iteration as in gridadmm_session_iterate. */
+gridadmm_status gridadmm_session_timed_steps(gridadmm_session* s, int n,
+                                             size_t flush_bytes,
+                                             double* step_ms, double* records);
+
 /* Total device time (ms) of the named kernel class since the session began,
  * measured with CUDA events on the session stream, and its launch count.
  * Classes: 0 gen, 1 branch, 2 bus, 3 zy (z+y+residual). */
@@ -128,6 +138,12 @@ gridadmm_status gridadmm_probe_tron_qp(int count, int n, const double* h,
                                        int* iterations);
 gridadmm_status gridadmm_probe_sincos(int n, const double* x, double* s,
                                       double* c);
+
+/* FP64 pipe microbenchmark on `device` (the branch kernel's roofline
+ * denominator): TFLOP/s issuing DMUL+DADD pairs (what -fmad=false code runs)
+ * and issuing DFMA. */
+gridadmm_status gridadmm_probe_fp64_peak(int device, double* tflops_mul_add,
+                                         double* tflops_fma);
 
 #ifdef __cplusplus
 }

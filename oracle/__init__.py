@@ -171,8 +171,9 @@ class RefNet:
                                       z_inf, prev_z_inf))
 
     def solve(self, init: Optional[Dict[str, np.ndarray]] = None, cap: int = 100000, **cfg):
-        """Full reference solve; returns (series[n, 5], info[9], final_state)."""
-        series = np.zeros(5 * cap)
+        """Full reference solve; returns (series[n, 6], info[9], final_state).
+        series columns: outer, inner, primal, dual, z_norm, elapsed_s."""
+        series = np.zeros(6 * cap)
         n = ctypes.c_int()
         info = np.zeros(9)
         fin = self.empty_state()
@@ -184,7 +185,7 @@ class RefNet:
         if rc != 0:
             raise RuntimeError(self.lib.ref_last_error().decode())
         k = min(n.value, cap)
-        return series[: 5 * k].reshape(-1, 5), info, fin
+        return series[: 6 * k].reshape(-1, 6), info, fin
 
 
 def ref_tron_qp(H, g, lo, hi, x0):

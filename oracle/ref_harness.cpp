@@ -217,8 +217,8 @@ long ref_phase(const void* netp, int phase, const double* cfgv,
 }
 
 // Full solve (proj/src/driver.cpp:140-246).  init may be NULL (cold start).
-// series receives up to cap records of 5 doubles (outer, inner, primal,
-// dual, z_norm); info receives status, outer, inner, failures, objective,
+// series receives up to cap records of 6 doubles (outer, inner, primal,
+// dual, z_norm, elapsed_s); info receives status, outer, inner, failures, objective,
 // balance_inf, limit_violation, bound_violation, c_inf (9 doubles).
 int ref_solve(const void* netp, const double* cfgv,
               const gridadmm_state_view* init, gridadmm_state_view* fin,
@@ -241,11 +241,12 @@ int ref_solve(const void* netp, const double* cfgv,
         if (nseries) *nseries = n;
         for (int k = 0; k < std::min(n, cap); ++k) {
             const IterationRecord& r = rep.series[k];
-            series[5 * k + 0] = r.outer;
-            series[5 * k + 1] = r.inner;
-            series[5 * k + 2] = r.primal_res;
-            series[5 * k + 3] = r.dual_res;
-            series[5 * k + 4] = r.z_norm;
+            series[6 * k + 0] = r.outer;
+            series[6 * k + 1] = r.inner;
+            series[6 * k + 2] = r.primal_res;
+            series[6 * k + 3] = r.dual_res;
+            series[6 * k + 4] = r.z_norm;
+            series[6 * k + 5] = r.elapsed_s;
         }
         if (info) {
             info[0] = static_cast<double>(rep.status);

@@ -84,12 +84,14 @@ EXT_SYMBOLS = {
     "gridadmm_session_set_state": (_I, [_P, ctypes.POINTER(StateView)]),
     "gridadmm_session_phase": (_I, [_P, _I, _DP]),
     "gridadmm_session_iterate": (_I, [_P, _I, _DP, _IP, _IP]),
-    "gridadmm_session_kernel_time": (_I, [_P, _I, _DP, ctypes.POINTER(ctypes.c_longlong)]),
+    "gridadmm_session_timed_steps": (_I, [_P, _I, ctypes.c_size_t, _DP, _DP]),
+    "gridadmm_session_kernel_time":(_I, [_P, _I, _DP, ctypes.POINTER(ctypes.c_longlong)]),
     "gridadmm_session_counters": (_I, [_P, ctypes.POINTER(ctypes.c_longlong),
                                        ctypes.POINTER(ctypes.c_longlong)]),
     "gridadmm_device_count": (_I, []),
     "gridadmm_probe_tron_qp": (_I, [_I, _I, _DP, _DP, _DP, _DP, _DP, _IP, _IP]),
     "gridadmm_probe_sincos": (_I, [_I, _DP, _DP, _DP]),
+    "gridadmm_probe_fp64_peak": (_I, [_I, _DP, _DP]),
 }
 
 
@@ -378,6 +380,13 @@ class Session:
                                               ctypes.byref(stop)))
         return rec[: 5 * done.value].reshape(-1, 5), stop.value
 
+    def timed_steps(self, n: int, flush_bytes: int = 0):
+        """n iterations, per-step device ms (CUDA events on the session stream)."""
+        ms = np.zeros(max(n, 1))
+        rec = np.zeros(5 * max(n, 1))
+        _check(lib().gridadmm_session_timed_steps(self._h, n, flush_bytes, _dp(ms), _dp(rec)))
+        return ms[:n], rec[: 5 * n].reshape(-1, 5)
+
     def kernel_time(self, cls: int):
         ms = _D()
         n = ctypes.c_longlong()
@@ -411,6 +420,13 @@ def probe_tron_qp(H, g, lo, hi, x0):
     _check(lib().gridadmm_probe_tron_qp(count, n, *[_dp(a) for a in args], _dp(x),
                                         status.ctypes.data_as(_IP), its.ctypes.data_as(_IP)))
     return x, status, its
+
+
+def fp64_peak(device: int = 0):
+    """(DMUL+DADD TFLOP/s, DFMA TFLOP/s) measured on the device."""
+    a, b = _D(), _D()
+    _check(lib().gridadmm_probe_fp64_peak(device, ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
 
 
 def probe_sincos(x):

@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(128) branch_kernel(DevNet net, DevState st, Br
                                                      const int* __restrict__ list, int count,
                                                      DevScalars* sc) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long my_iters = 0, my_sincos = 0;
+    unsigned long long my_iters = 0;
     int my_fail = 0;
     if (idx < count) {
         const int b = list[idx];
@@ -370,7 +370,6 @@ __global__ void __launch_bounds__(128) branch_kernel(DevNet net, DevState st, Br
                 branch_flows(p.yc, pt[0], pt[1], pt[2], pt[3], fl);
                 const double rij = fl[0] * fl[0] + fl[1] * fl[1] + pt[4];
                 const double rji = fl[2] * fl[2] + fl[3] * fl[3] + pt[5];
-                my_sincos += 1;
                 const double res = smax(fabs(rij), fabs(rji));
                 if (res <= kAlTol) break;
                 p.lt_ij = sclamp(p.lt_ij + p.rho_t * rij, -kLtBound, kLtBound);
@@ -391,7 +390,6 @@ __global__ void __launch_bounds__(128) branch_kernel(DevNet net, DevState st, Br
         for (int k = 0; k < 6; ++k) st.bp[k * net.nl + b] = pt[k];
         double fl[4];
         branch_flows(p.yc, pt[0], pt[1], pt[2], pt[3], fl);
-        my_sincos += 1;
         const int base = 2 * net.ng + 8 * b;
         st.x[base + 0] = fl[0];
         st.x[base + 1] = fl[1];
@@ -410,7 +408,7 @@ __global__ void __launch_bounds__(128) branch_kernel(DevNet net, DevState st, Br
         my_fail += __shfl_down_sync(full, my_fail, o);
     }
     if ((threadIdx.x & 31) == 0) {
-        if (my_iters) atomicAdd(&sc->tron_iters, my_iters);
+        if (my_iters) atomicAdd(N == 6 ? &sc->tron_iters6 : &sc->tron_iters4, my_iters);
         if (my_fail) atomicAdd(&sc->failures, (unsigned long long)my_fail);
     }
 }

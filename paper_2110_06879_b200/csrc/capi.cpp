@@ -449,6 +449,15 @@ gridadmm_status gridadmm_session_iterate(gridadmm_session* s, int n, double* rec
     });
 }
 
+gridadmm_status gridadmm_session_timed_steps(gridadmm_session* s, int n, size_t flush_bytes,
+                                             double* step_ms, double* records) {
+    if (!s || n < 0) return fail(GRIDADMM_ERR_INVALID_ARG, "bad argument to session_timed_steps");
+    return guarded([&]() -> gridadmm_status {
+        s->s->timed_steps(n, flush_bytes, step_ms, records);
+        return GRIDADMM_OK;
+    });
+}
+
 gridadmm_status gridadmm_session_kernel_time(const gridadmm_session* s, int cls, double* ms,
                                              long long* launches) {
     if (!s || cls < 0 || cls > 3) return fail(GRIDADMM_ERR_INVALID_ARG, "bad argument to kernel_time");
@@ -500,6 +509,19 @@ gridadmm_status gridadmm_probe_tron_qp(int count, int n, const double* h, const 
         ck(cudaMemcpy(status, ds, count * 4, cudaMemcpyDeviceToHost));
         ck(cudaMemcpy(iterations, di, count * 4, cudaMemcpyDeviceToHost));
         for (void* p : {(void*)dh, (void*)dg, (void*)dl, (void*)du, (void*)dx, (void*)ds, (void*)di}) cudaFree(p);
+        return GRIDADMM_OK;
+    });
+}
+
+gridadmm_status gridadmm_probe_fp64_peak(int device, double* tflops_mul_add, double* tflops_fma) {
+    return guarded([&]() -> gridadmm_status {
+        if (cudaSetDevice(device) != cudaSuccess) throw ga::CudaError("cudaSetDevice");
+        double a = 0.0, b = 0.0;
+        ga::measure_fp64_peak(&a, &b);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) throw ga::CudaError(cudaGetErrorString(e));
+        if (tflops_mul_add) *tflops_mul_add = a;
+        if (tflops_fma) *tflops_fma = b;
         return GRIDADMM_OK;
     });
 }

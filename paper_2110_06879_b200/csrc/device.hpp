@@ -59,8 +59,8 @@ struct DevScalars {
     unsigned long long z_inf;       // max |z|
     unsigned long long z_drift;     // max |z - z_prev|
     unsigned long long failures;    // branch NumericalError count
-    unsigned long long tron_iters;  // TRON iterations executed (census)
-    unsigned long long sincos;      // sincos evaluations (census)
+    unsigned long long tron_iters4; // TRON iterations, unlimited (4-var) branches
+    unsigned long long tron_iters6; // TRON iterations, rate-limited (6-var) branches
     int singular_bus;               // min singular bus index, INT_MAX if none
     int pad;
 };
@@ -96,6 +96,8 @@ void launch_clamp_gen_p(const DevNet& n, const DevState& s, cudaStream_t st);
 void launch_tron_qp(int count, int n, const double* h, const double* g,
                     const double* l, const double* u, double* x, int* status,
                     int* iterations, cudaStream_t st);
+// FP64 pipe peak (TFLOP/s) for DMUL+DADD (no FMA) and DFMA issue.
+void measure_fp64_peak(double* tflops_mul_add, double* tflops_fma);
 // Pinned sincos on the device (parity probe).
 void launch_sincos_probe(const double* x, double* s, double* c, int n, cudaStream_t st);
 

@@ -327,7 +327,60 @@ __global__ void reset_scalars_kernel(DevScalars* sc) {
 
 inline int blocks_for(int n) { return (n + kBlock - 1) / kBlock; }
 
+// FP64 pipe microbenchmark: 8 independent chains per thread.  kFma = false
+// issues DMUL + DADD (what -fmad=false code runs), true issues DFMA.
+template <bool kFma>
+__global__ void __launch_bounds__(kBlock) fp64_peak_kernel(double* out, int iters, double b,
+                                                            double c) {
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = threadIdx.x * 1e-9 + k;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (kFma) a[k] = fma(a[k], b, c);
+            else a[k] = a[k] * b + c;
+        }
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += a[k];
+    if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
 }  // namespace
+
+void measure_fp64_peak(double* tflops_mul_add, double* tflops_fma) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    double* out = nullptr;
+    cudaMalloc(&out, sizeof(double));
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const int blocks = sms * 8, iters = 4096;
+    const double flops = 2.0 * 8.0 * iters * blocks * (double)kBlock;
+    for (int pass = 0; pass < 2; ++pass) {
+        float best = 1e30f;
+        for (int rep = 0; rep < 5; ++rep) {
+            cudaEventRecord(a);
+            if (pass == 0) fp64_peak_kernel<false><<<blocks, kBlock>>>(out, iters, 0.999999, 1e-7);
+            else fp64_peak_kernel<true><<<blocks, kBlock>>>(out, iters, 0.999999, 1e-7);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float ms = 0.0f;
+            cudaEventElapsedTime(&ms, a, b);
+            if (ms < best) best = ms;
+        }
+        const double tf = flops / (best * 1e-3) / 1e12;
+        if (pass == 0) *tflops_mul_add = tf;
+        else *tflops_fma = tf;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(out);
+}
 
 void launch_generators(const DevNet& n, const DevState& s, cudaStream_t st) {
     if (n.ng > 0) gen_kernel<<<blocks_for(n.ng), kBlock, 0, st>>>(n, s);

@@ -54,6 +54,8 @@ void Session::free_all() {
     if (sc_) cudaFree(sc_);
     if (red_) cudaFree(red_);
     if (sc_host_) cudaFreeHost(sc_host_);
+    if (flush_buf_) cudaFree(flush_buf_);
+    flush_buf_ = nullptr;
     sc_ = nullptr;
     red_ = nullptr;
     sc_host_ = nullptr;
@@ -304,7 +306,37 @@ long Session::run_phase(int phase, double z_inf, double prev_z_inf) {
     return ret;
 }
 
-int Session::iterate(double out[4], PhaseTimes* times) {
+int Session::timed_steps(int k, size_t flush_bytes, double* step_ms, double* records) {
+    if (flush_bytes > flush_size_) {
+        if (flush_buf_) cudaFree(flush_buf_);
+        flush_buf_ = nullptr;
+        check(cudaMalloc(&flush_buf_, flush_bytes), "cudaMalloc flush");
+        flush_size_ = flush_bytes;
+    }
+    cudaEvent_t a, b;
+    check(cudaEventCreate(&a), "event");
+    check(cudaEventCreate(&b), "event");
+    const double rmax = rho_max();
+    int done = 0;
+    for (; done < k; ++done) {
+        if (flush_bytes) check(cudaMemsetAsync(flush_buf_, done & 0xff, flush_bytes, stream_), "flush");
+        cudaEventRecord(a, stream_);
+        double nrm[4];
+        const int fails = iterate(nrm, nullptr, b);
+        float ms = 0.0f;
+        cudaEventElapsedTime(&ms, a, b);
+        if (step_ms) step_ms[done] = ms;
+        if (records) {
+            double* r = records + 5 * done;
+            r[0] = nrm[0]; r[1] = nrm[1] * rmax; r[2] = nrm[2]; r[3] = nrm[3]; r[4] = fails;
+        }
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return done;
+}
+
+int Session::iterate(double out[4], PhaseTimes* times, cudaEvent_t end_event) {
     launch_reset_scalars(sc_, stream_);
     cudaEventRecord(ev_[0], stream_);
     launch_generators(dn_, ds_, stream_);
@@ -317,6 +349,7 @@ int Session::iterate(double out[4], PhaseTimes* times) {
     cudaEventRecord(ev_[4], stream_);
     check(cudaGetLastError(), "iteration launch");
     check(cudaMemcpyAsync(sc_host_, sc_, sizeof(DevScalars), cudaMemcpyDeviceToHost, stream_), "D2H");
+    if (end_event) cudaEventRecord(end_event, stream_);
     check(cudaStreamSynchronize(stream_), "iteration sync");
     float ms[4] = {0, 0, 0, 0};
     for (int k = 0; k < 4; ++k) {
@@ -358,13 +391,13 @@ double Session::rho_max() {
 long long Session::tron_iterations() const {
     DevScalars h;
     check(cudaMemcpy(&h, sc_, sizeof h, cudaMemcpyDeviceToHost), "D2H");
-    return static_cast<long long>(h.tron_iters);
+    return static_cast<long long>(h.tron_iters4);
 }
 
 long long Session::sincos_calls() const {
     DevScalars h;
     check(cudaMemcpy(&h, sc_, sizeof h, cudaMemcpyDeviceToHost), "D2H");
-    return static_cast<long long>(h.sincos);
+    return static_cast<long long>(h.tron_iters6);
 }
 
 void Session::sync() const { check(cudaStreamSynchronize(stream_), "sync"); }

@@ -127,7 +127,13 @@ public:
     // the scalars.  Fills out[0..3] = primal_inf, dual_inf (raw, before
     // rho_max), z_inf, z_drift; returns branch failures; throws
     // SingularBusError.
-    int iterate(double out[4], PhaseTimes* times);
+    int iterate(double out[4], PhaseTimes* times, cudaEvent_t end_event = nullptr);
+
+    // Benchmark helper: k iterations, each bracketed by CUDA events on the
+    // session stream (launches through the D2H of its norms); an L2 flush of
+    // flush_bytes runs between steps outside the brackets.  records gets 5
+    // doubles per step (primal, dual, z, z_drift, failures).
+    int timed_steps(int k, size_t flush_bytes, double* step_ms, double* records);
     void outer_update();                       // lambda clamp on the device
     double rho_max();                          // max over rows, device reduction
 
@@ -150,6 +156,8 @@ private:
     DevScalars* sc_ = nullptr;       // device
     DevScalars* sc_host_ = nullptr;  // pinned mirror
     unsigned long long* red_ = nullptr;
+    void* flush_buf_ = nullptr;
+    size_t flush_size_ = 0;
     double beta_ = 0.0;
     cudaStream_t stream_ = nullptr;
     cudaEvent_t ev_[5] = {};

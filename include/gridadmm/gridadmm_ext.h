@@ -123,6 +123,16 @@ gridadmm_status gridadmm_session_counters(const gridadmm_session* s,
                                           long long* tron_iterations,
                                           long long* sincos_calls);
 
+/* TRON iterations each branch took in the last branch sweep (num_branches
+ * ints) — the LPT scheduling key, exposed for profiling. */
+gridadmm_status gridadmm_session_branch_costs(const gridadmm_session* s, int* costs);
+
+/* TRON path counters since the last reset (8 values: steps, Cauchy
+ * extrapolations, Cauchy halvings, CG iterations, line-search steps, failed
+ * preconditioners, -, -); all zero unless the library was built with
+ * -DGA_TRON_STATS (`make stats`). */
+gridadmm_status gridadmm_debug_tron_stats(unsigned long long* out, int reset);
+
 /* Number of CUDA devices visible to the library. */
 int gridadmm_device_count(void);
 

@@ -25,7 +25,7 @@ __all__ = [
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 REPO_DIR = os.path.dirname(PKG_DIR)
-LIB_PATH = os.path.join(PKG_DIR, "libgridadmm.so")
+LIB_PATH = os.environ.get("GRIDADMM_LIB", os.path.join(PKG_DIR, "libgridadmm.so"))
 
 STATUS = {
     0: "OK", 1: "ERR_IO", 2: "ERR_PARSE", 3: "ERR_INVALID_ARG", 4: "ERR_ITERATION_LIMIT",
@@ -89,6 +89,8 @@ EXT_SYMBOLS = {
     "gridadmm_session_counters": (_I, [_P, ctypes.POINTER(ctypes.c_longlong),
                                        ctypes.POINTER(ctypes.c_longlong)]),
     "gridadmm_device_count": (_I, []),
+    "gridadmm_session_branch_costs": (_I, [_P, _IP]),
+    "gridadmm_debug_tron_stats": (_I, [ctypes.POINTER(ctypes.c_ulonglong), _I]),
     "gridadmm_probe_tron_qp": (_I, [_I, _I, _DP, _DP, _DP, _DP, _DP, _IP, _IP]),
     "gridadmm_probe_sincos": (_I, [_I, _DP, _DP, _DP]),
     "gridadmm_probe_fp64_peak": (_I, [_I, _DP, _DP]),
@@ -392,6 +394,11 @@ class Session:
         n = ctypes.c_longlong()
         _check(lib().gridadmm_session_kernel_time(self._h, cls, ctypes.byref(ms), ctypes.byref(n)))
         return ms.value, n.value
+
+    def branch_costs(self) -> np.ndarray:
+        out = np.zeros(max(1, self.shapes["lt_ij"]), dtype=np.int32)
+        _check(lib().gridadmm_session_branch_costs(self._h, out.ctypes.data_as(_IP)))
+        return out[: self.shapes["lt_ij"]]
 
     def counters(self):
         t = ctypes.c_longlong()

@@ -3,7 +3,25 @@
 // TRON solve of the 4- or 6-variable branch subproblem (Eq. 4 of the paper).
 //
 // Reference semantics: proj/src/kernels.cpp:17-192 (BranchProblem, eval,
-// consensus values) and :211-292 (solve_branch_batch).  Bit-exactness notes:
+// consensus values) and :211-292 (solve_branch_batch).
+//
+// Scheduling (the B200 design; the reference's is a static block partition
+// over threads, proj/src/parallel.hpp:13-33): the TRON cost per branch is
+// heavy-tailed (median 2-3 iterations, 10-40% at the 200 cap), so a
+// thread-per-branch grid leaves whole warps waiting on one capped branch.
+// Instead a persistent grid of warps drains two work queues (rate-limited
+// 6-variable branches, unlimited 4-variable ones), each ordered by the
+// branch's TRON iteration count in the previous sweep, longest first
+// (LPT).  Each lane owns one branch at a time and advances it ONE trust-region
+// iteration per loop trip; when its solve ends (converged / cap / error /
+// AL round done) the lane finalizes the branch and immediately refills from
+// the queue with a warp-aggregated atomic, so lanes stay busy until the queue
+// is empty.  Per-lane problem data (48 doubles) lives in shared memory in a
+// [field][lane] layout (conflict-free), the TRON iterate and all per-iteration
+// vectors/matrices in registers.  Results do not depend on the schedule: each
+// branch's arithmetic is identical wherever it runs.
+//
+// Bit-exactness notes:
 //  * eval accumulation order is the reference's: rows 0-3 (flows), 4 (w_i),
 //    6 (w_j), then the angle rows 5, 7, then limit ij, limit ji
 //    (kernels.cpp:124-162);
@@ -24,6 +42,19 @@
 
 namespace ga {
 
+void tron_stats(unsigned long long out[8], bool reset) {
+#ifdef GA_TRON_STATS
+    cudaMemcpyFromSymbol(out, g_tron_stats, 8 * sizeof(unsigned long long));
+    if (reset) {
+        const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_tron_stats, z, sizeof z);
+    }
+#else
+    (void)reset;
+    for (int k = 0; k < 8; ++k) out[k] = 0;
+#endif
+}
+
 namespace {
 
 constexpr double kTwoPi = 6.283185307179586;  // 2.0 * std::numbers::pi
@@ -32,6 +63,29 @@ constexpr int kMaxAl = 10;                    // kernels.cpp:219
 constexpr double kAlTol = 1e-8;
 constexpr double kAlShrink = 0.25;
 constexpr double kRhoTildeMax = 1e7;
+
+constexpr int kBranchBlock = 128;  // threads per block of the persistent kernel
+constexpr int kCostBuckets = 256;  // LPT ordering buckets (cost >> 2, capped)
+
+// ---- per-lane problem data in shared memory ------------------------------
+// Field indices of the [field][lane] layout.
+enum Field : int {
+    F_YC = 0,     // 8 admittance coefficients gii bii gij bij gji bji gjj bjj
+    F_TGT = 8,    // 8 bus-side targets (xbar rows)
+    F_Y = 16,     // 8 multipliers y
+    F_Z = 24,     // 8 artificial z
+    F_RHO = 32,   // 8 penalties
+    F_LTIJ = 40, F_LTJI = 41, F_RHOT = 42,
+    F_VMIN_I = 43, F_VMAX_I = 44, F_VMIN_J = 45, F_VMAX_J = 46, F_R2 = 47,
+    kFields = 48
+};
+
+template <int BS>
+struct Slot {
+    double* p;  // smem + threadIdx.x
+    GA_FN double operator()(int f) const { return p[f * BS]; }
+    GA_FN void set(int f, double v) const { p[f * BS] = v; }
+};
 
 // Flow quantities (value, gradient over vi,vj,thi,thj, Hessian) of the four
 // branch flows in BranchRow order, built from the basis functions
@@ -99,12 +153,12 @@ GA_FN double wim_h(const Basis& b, int i, int j) {
 
 // Flow k uses A = wi (k < 2, index a = 0) or wj (k >= 2, a = 1) and the
 // coefficients of flow_quads (kernels.cpp:80-87).
-template <bool WG, bool WH>
-GA_FN void make_flows(const Basis& b, const double* yc, Flows& F) {
-    // yc: gii bii gij bij gji bji gjj bjj
-    const double ca[4] = {yc[0], -yc[1], yc[6], -yc[7]};
-    const double cb[4] = {yc[2], -yc[3], yc[4], -yc[5]};
-    const double cc[4] = {yc[3], yc[2], -yc[5], -yc[4]};
+template <bool WG, bool WH, class Y>
+GA_FN void make_flows(const Basis& b, const Y& yc, Flows& F) {
+    // yc(k): gii bii gij bij gji bji gjj bjj
+    const double ca[4] = {yc(0), -yc(1), yc(6), -yc(7)};
+    const double cb[4] = {yc(2), -yc(3), yc(4), -yc(5)};
+    const double cc[4] = {yc(3), yc(2), -yc(5), -yc(4)};
     const double wi_v = b.vi * b.vi, wj_v = b.vj * b.vj;
     const double wr_v = b.vivj * b.c, wim_v = b.vivj * b.s;
 #pragma unroll
@@ -140,26 +194,39 @@ GA_FN bool flow_h_zero(int k, int i, int j) {
     return i == na && j == na;
 }
 
-// Row targets / multipliers / artificial values / penalties in BranchRow order.
-struct RowData {
-    double tgt[8], yv[8], zv[8], rh[8];
+template <int BS>
+struct YcView {
+    Slot<BS> s;
+    GA_FN double operator()(int k) const { return s(F_YC + k); }
 };
 
-template <int N>
+// The branch subproblem over a shared-memory slot (kernels.cpp:17-163).
+template <int N, int BS>
 struct BranchProb {
     static constexpr bool kLimited = N == 6;
-    double lo_[N], hi_[N];
-    double yc[8];
-    RowData r;
-    double lt_ij, lt_ji, rho_t;
+    Slot<BS> s;
     mutable double cc_, ss_;  // sincos at the last gradient point
 
-    GA_FN double lo(int i) const { return lo_[i]; }
-    GA_FN double hi(int i) const { return hi_[i]; }
+    GA_FN double lo(int i) const {
+        switch (i) {
+            case 0: return s(F_VMIN_I);
+            case 1: return s(F_VMIN_J);
+            case 2: case 3: return -kTwoPi;
+            default: return -s(F_R2);
+        }
+    }
+    GA_FN double hi(int i) const {
+        switch (i) {
+            case 0: return s(F_VMAX_I);
+            case 1: return s(F_VMAX_J);
+            case 2: case 3: return kTwoPi;
+            default: return 0.0;
+        }
+    }
 
     // f, g, H of Eq. (4) at x (kernels.cpp:103-163).
     template <bool WF, bool WG, bool WH>
-    GA_FN void eval(const double* x, double c, double s, double* f, double* g, double* h) const {
+    GA_FN void eval(const double* x, double c, double sn, double* f, double* g, double* h) const {
         if (WF) *f = 0.0;
         if (WG) {
 #pragma unroll
@@ -169,16 +236,17 @@ struct BranchProb {
 #pragma unroll
             for (int i = 0; i < N * N; ++i) h[i] = 0.0;
         }
-        const Basis b = make_basis(x[0], x[1], c, s);
+        const Basis b = make_basis(x[0], x[1], c, sn);
         Flows F;
-        make_flows<WG, WH>(b, yc, F);
+        make_flows<WG, WH>(b, YcView<BS>{s}, F);
 
         // flows, rows 0..3
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const double d = F.v[k] - r.tgt[k] + r.zv[k];
-            const double w = r.yv[k] + r.rh[k] * d;
-            if (WF) *f += r.yv[k] * d + 0.5 * r.rh[k] * d * d;
+            const double rh = s(F_RHO + k), yv = s(F_Y + k);
+            const double d = F.v[k] - s(F_TGT + k) + s(F_Z + k);
+            const double w = yv + rh * d;
+            if (WF) *f += yv * d + 0.5 * rh * d * d;
             if (WG) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) g[i] += w * F.g[k][i];
@@ -188,7 +256,7 @@ struct BranchProb {
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        const double gg = r.rh[k] * F.g[k][i] * F.g[k][j];
+                        const double gg = rh * F.g[k][i] * F.g[k][j];
                         if (flow_h_zero(k, i, j)) h[i * N + j] += gg;
                         else h[i * N + j] += w * F.h[k][i * 4 + j] + gg;
                     }
@@ -202,75 +270,79 @@ struct BranchProb {
             const double v = x[a];
             const double ev = v * v;
             const double eg = 2 * v;
-            const double d = ev - r.tgt[row] + r.zv[row];
-            const double w = r.yv[row] + r.rh[row] * d;
-            if (WF) *f += r.yv[row] * d + 0.5 * r.rh[row] * d * d;
+            const double rh = s(F_RHO + row), yv = s(F_Y + row);
+            const double d = ev - s(F_TGT + row) + s(F_Z + row);
+            const double w = yv + rh * d;
+            if (WF) *f += yv * d + 0.5 * rh * d * d;
             if (WG) g[a] += w * eg;
-            if (WH) h[a * N + a] += w * 2.0 + r.rh[row] * eg * eg;
+            if (WH) h[a * N + a] += w * 2.0 + rh * eg * eg;
         }
         // angle rows 5 (thi, var 2) and 7 (thj, var 3) are linear
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
             const int row = t == 0 ? 5 : 7;
             const int i = 2 + t;
-            const double d = x[i] - r.tgt[row] + r.zv[row];
-            if (WF) *f += r.yv[row] * d + 0.5 * r.rh[row] * d * d;
-            if (WG) g[i] += r.yv[row] + r.rh[row] * d;
-            if (WH) h[i * N + i] += r.rh[row];
+            const double rh = s(F_RHO + row), yv = s(F_Y + row);
+            const double d = x[i] - s(F_TGT + row) + s(F_Z + row);
+            if (WF) *f += yv * d + 0.5 * rh * d * d;
+            if (WG) g[i] += yv + rh * d;
+            if (WH) h[i * N + i] += rh;
         }
-        if (!kLimited) return;
-        // line-limit AL terms: res = p^2 + q^2 + s (kernels.cpp:146-162)
+        if constexpr (kLimited) {
+            const double rho_t = s(F_RHOT);
+            // line-limit AL terms: res = p^2 + q^2 + s (kernels.cpp:146-162)
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-            const int kp = t == 0 ? 0 : 2, kq = kp + 1;
-            const int srow = 4 + t;
-            const double lt = t == 0 ? lt_ij : lt_ji;
-            const double pv = F.v[kp], qv = F.v[kq];
-            const double res = pv * pv + qv * qv + x[srow];
-            const double w = lt + rho_t * res;
-            if (WF) *f += lt * res + 0.5 * rho_t * res * res;
-            if (WG || WH) {
-                double gr[4];
+            for (int t = 0; t < 2; ++t) {
+                const int kp = t == 0 ? 0 : 2, kq = kp + 1;
+                const int srow = 4 + t;
+                const double lt = s(t == 0 ? F_LTIJ : F_LTJI);
+                const double pv = F.v[kp], qv = F.v[kq];
+                const double res = pv * pv + qv * qv + x[srow];
+                const double w = lt + rho_t * res;
+                if (WF) *f += lt * res + 0.5 * rho_t * res * res;
+                if (WG || WH) {
+                    double gr[4];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) gr[i] = 2 * pv * F.g[kp][i] + 2 * qv * F.g[kq][i];
-                if (WG) {
+                    for (int i = 0; i < 4; ++i) gr[i] = 2 * pv * F.g[kp][i] + 2 * qv * F.g[kq][i];
+                    if (WG) {
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) g[i] += w * gr[i];
-                    g[srow] += w * 1.0;
-                }
-                if (WH) {
-                    const double w2 = w * 2.0;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            double acc;
-                            if (flow_h_zero(kp, i, j))
-                                acc = F.g[kp][i] * F.g[kp][j] + F.g[kq][i] * F.g[kq][j];
-                            else
-                                acc = F.g[kp][i] * F.g[kp][j] + pv * F.h[kp][i * 4 + j] +
-                                      F.g[kq][i] * F.g[kq][j] + qv * F.h[kq][i * 4 + j];
-                            h[i * N + j] += w2 * acc;
-                        }
-                    // rho_t * gr gr' over all n with gr[srow] = 1, other slack 0
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) h[i * N + j] += rho_t * gr[i] * gr[j];
-                        h[i * N + srow] += rho_t * gr[i] * 1.0;
+                        for (int i = 0; i < 4; ++i) g[i] += w * gr[i];
+                        g[srow] += w * 1.0;
                     }
+                    if (WH) {
+                        const double w2 = w * 2.0;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) h[srow * N + j] += rho_t * 1.0 * gr[j];
-                    h[srow * N + srow] += rho_t * 1.0 * 1.0;
+                        for (int i = 0; i < 4; ++i)
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                double acc;
+                                if (flow_h_zero(kp, i, j))
+                                    acc = F.g[kp][i] * F.g[kp][j] + F.g[kq][i] * F.g[kq][j];
+                                else
+                                    acc = F.g[kp][i] * F.g[kp][j] + pv * F.h[kp][i * 4 + j] +
+                                          F.g[kq][i] * F.g[kq][j] + qv * F.h[kq][i * 4 + j];
+                                h[i * N + j] += w2 * acc;
+                            }
+                        // rho_t * gr gr' over all n with gr[srow] = 1, other slack 0
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) h[i * N + j] += rho_t * gr[i] * gr[j];
+                            h[i * N + srow] += rho_t * gr[i] * 1.0;
+                        }
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) h[srow * N + j] += rho_t * 1.0 * gr[j];
+                        h[srow * N + srow] += rho_t * 1.0 * 1.0;
+                    }
                 }
             }
         }
     }
 
     GA_FN double value(const double* x) const {
-        double c, s, f;
-        ga_sincos(x[2] - x[3], &s, &c);
-        eval<true, false, false>(x, c, s, &f, nullptr, nullptr);
+        double c, sn, f;
+        ga_sincos(x[2] - x[3], &sn, &c);
+        eval<true, false, false>(x, c, sn, &f, nullptr, nullptr);
         return f;
     }
     GA_FN void gradient(const double* x, double* g) const {
@@ -284,132 +356,248 @@ struct BranchProb {
 };
 
 // branch_flows (netdata.cpp:33-45)
-GA_FN void branch_flows(const double* yc, double vi, double vj, double thi, double thj,
-                        double* out) {
+template <class Y>
+GA_FN void branch_flows(const Y& yc, double vi, double vj, double thi, double thj, double* out) {
     double s, c;
     ga_sincos(thi - thj, &s, &c);
     const double wi = vi * vi, wj = vj * vj;
     const double wr = vi * vj * c, wim = vi * vj * s;
-    out[0] = yc[0] * wi + yc[2] * wr + yc[3] * wim;     // pij
-    out[1] = -yc[1] * wi - yc[3] * wr + yc[2] * wim;    // qij
-    out[2] = yc[6] * wj + yc[4] * wr - yc[5] * wim;     // pji
-    out[3] = -yc[7] * wj - yc[5] * wr - yc[4] * wim;    // qji
+    out[0] = yc(0) * wi + yc(2) * wr + yc(3) * wim;     // pij
+    out[1] = -yc(1) * wi - yc(3) * wr + yc(2) * wim;    // qij
+    out[2] = yc(6) * wj + yc(4) * wr - yc(5) * wim;     // pji
+    out[3] = -yc(7) * wj - yc(5) * wr - yc(4) * wim;    // qji
 }
 
-template <int N>
-__device__ void load_problem(const DevNet& net, const DevState& st, const BranchCfg& cfg,
-                             int b, BranchProb<N>& p) {
+// Fills this lane's slot for branch b (kernels.cpp:229-241).
+template <int BS>
+__device__ __forceinline__ void load_slot(const DevNet& net, const DevState& st,
+                                          const BranchCfg& cfg, int b, Slot<BS> s) {
     const int from = net.br_from[b], to = net.br_to[b];
-    p.lo_[0] = net.b_vmin[from];
-    p.lo_[1] = net.b_vmin[to];
-    p.lo_[2] = -kTwoPi;
-    p.lo_[3] = -kTwoPi;
-    p.hi_[0] = net.b_vmax[from];
-    p.hi_[1] = net.b_vmax[to];
-    p.hi_[2] = kTwoPi;
-    p.hi_[3] = kTwoPi;
-    if constexpr (N == 6) {
-        const double rt = cfg.limit_tighten * net.br_rate[b];
-        const double r2 = rt * rt;
-        p.lo_[4] = -r2;
-        p.lo_[5] = -r2;
-        p.hi_[4] = 0.0;
-        p.hi_[5] = 0.0;
-    }
 #pragma unroll
-    for (int k = 0; k < 8; ++k) p.yc[k] = net.br_y[k * net.nl + b];
+    for (int k = 0; k < 8; ++k) s.set(F_YC + k, __ldg(&net.br_y[k * net.nl + b]));
     const int base = 2 * net.ng + 8 * b;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-        p.r.tgt[k] = st.xbar[base + k];
-        p.r.yv[k] = st.y[base + k];
-        p.r.zv[k] = st.z[base + k];
-        p.r.rh[k] = st.rho[base + k];
+        s.set(F_TGT + k, st.xbar[base + k]);
+        s.set(F_Y + k, st.y[base + k]);
+        s.set(F_Z + k, st.z[base + k]);
+        s.set(F_RHO + k, st.rho[base + k]);
     }
-    p.lt_ij = st.lt_ij[b];
-    p.lt_ji = st.lt_ji[b];
-    p.rho_t = st.rho_t[b];
+    s.set(F_LTIJ, st.lt_ij[b]);
+    s.set(F_LTJI, st.lt_ji[b]);
+    s.set(F_RHOT, st.rho_t[b]);
+    s.set(F_VMIN_I, __ldg(&net.b_vmin[from]));
+    s.set(F_VMAX_I, __ldg(&net.b_vmax[from]));
+    s.set(F_VMIN_J, __ldg(&net.b_vmin[to]));
+    s.set(F_VMAX_J, __ldg(&net.b_vmax[to]));
+    const double rt = cfg.limit_tighten * __ldg(&net.br_rate[b]);
+    s.set(F_R2, rt * rt);
 }
 
-// One thread per branch (kernels.cpp:229-282).
-template <int N>
-__global__ void __launch_bounds__(128) branch_kernel(DevNet net, DevState st, BranchCfg cfg,
-                                                     const int* __restrict__ list, int count,
-                                                     DevScalars* sc) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+struct Queue {
+    const int* order;  // branch indices, longest expected first
+    int count;
+    int* counter;      // next index to hand out
+};
+
+// Drains one queue with per-lane refill (see file header).
+template <int N, int BS>
+__device__ __noinline__ void drain_queue(const DevNet& net, const DevState& st,
+                                         const BranchCfg& cfg, const Queue q, int* cost,
+                                         double* smem, unsigned long long* iters_out,
+                                         int* fail_out) {
+    constexpr unsigned kFull = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const Slot<BS> slot{smem + threadIdx.x};
+    BranchProb<N, BS> p{slot};
+    TronParams tp;
+    tp.gtol = cfg.gtol;
+    tp.max_iterations = cfg.max_iterations;
+    tp.cg_tol = cfg.cg_tol;
+    tp.max_cg = cfg.max_cg;
+    tp.delta_floor = cfg.delta_floor;
+    const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+
+    TronState<N> ts;
+    int b = -1;
+    bool exhausted = false;
+    int al_it = 0, iters = 0;
+    double prev_res = kInf;
     unsigned long long my_iters = 0;
     int my_fail = 0;
-    if (idx < count) {
-        const int b = list[idx];
-        BranchProb<N> p;
-        load_problem<N>(net, st, cfg, b, p);
-        TronParams tp;
-        tp.gtol = cfg.gtol;
-        tp.max_iterations = cfg.max_iterations;
-        tp.cg_tol = cfg.cg_tol;
-        tp.max_cg = cfg.max_cg;
-        tp.delta_floor = cfg.delta_floor;
 
-        double prev[6], pt[6];
+    // Branch done: restore on failure, write back (kernels.cpp:273-281).
+    auto finalize = [&](bool failed) {
+        double pt[6];
 #pragma unroll
-        for (int k = 0; k < 6; ++k) prev[k] = pt[k] = st.bp[k * net.nl + b];
-        bool failed = false;
-        if constexpr (N == 4) {
-            int its = 0;
-            const int status = tron_solve<4>(p, pt, tp, &its);
-            failed = status == kTronNumericalError;
-            my_iters += its;
-        } else {
-            double prev_res = __longlong_as_double(0x7ff0000000000000LL);  // +inf
-            for (int it = 0; it < kMaxAl; ++it) {
-                int its = 0;
-                const int status = tron_solve<6>(p, pt, tp, &its);
-                my_iters += its;
-                if (status == kTronNumericalError) { failed = true; break; }
+        for (int k = 0; k < N; ++k) pt[k] = failed ? st.bp[k * net.nl + b] : ts.x[k];
+        st.lt_ij[b] = slot(F_LTIJ);
+        st.lt_ji[b] = slot(F_LTJI);
+        st.rho_t[b] = slot(F_RHOT);
+        if (!failed) {
+#pragma unroll
+            for (int k = 0; k < N; ++k) st.bp[k * net.nl + b] = pt[k];
+        }
+        double fl[4];
+        branch_flows(YcView<BS>{slot}, pt[0], pt[1], pt[2], pt[3], fl);
+        const int base = 2 * net.ng + 8 * b;
+        double2* xr = reinterpret_cast<double2*>(st.x + base);
+        xr[0] = make_double2(fl[0], fl[1]);
+        xr[1] = make_double2(fl[2], fl[3]);
+        xr[2] = make_double2(pt[0] * pt[0], pt[2]);
+        xr[3] = make_double2(pt[1] * pt[1], pt[3]);
+        cost[b] = iters;
+        my_iters += iters;
+        my_fail += failed ? 1 : 0;
+        b = -1;
+    };
+    // A TRON solve ended with `status`: AL bookkeeping (kernels.cpp:246-271);
+    // either restarts TRON for the next AL round or finalizes the branch.
+    auto after_solve = [&](int status) {
+        for (;;) {
+            if (status == kTronNumericalError) { finalize(true); return; }
+            if constexpr (N == 4) {
+                finalize(false);
+                return;
+            } else {
                 double fl[4];
-                branch_flows(p.yc, pt[0], pt[1], pt[2], pt[3], fl);
-                const double rij = fl[0] * fl[0] + fl[1] * fl[1] + pt[4];
-                const double rji = fl[2] * fl[2] + fl[3] * fl[3] + pt[5];
+                branch_flows(YcView<BS>{slot}, ts.x[0], ts.x[1], ts.x[2], ts.x[3], fl);
+                const double rij = fl[0] * fl[0] + fl[1] * fl[1] + ts.x[4];
+                const double rji = fl[2] * fl[2] + fl[3] * fl[3] + ts.x[5];
                 const double res = smax(fabs(rij), fabs(rji));
-                if (res <= kAlTol) break;
-                p.lt_ij = sclamp(p.lt_ij + p.rho_t * rij, -kLtBound, kLtBound);
-                p.lt_ji = sclamp(p.lt_ji + p.rho_t * rji, -kLtBound, kLtBound);
-                if (res > kAlShrink * prev_res) p.rho_t = smin(10.0 * p.rho_t, kRhoTildeMax);
+                if (res <= kAlTol) { finalize(false); return; }
+                const double rho_t = slot(F_RHOT);
+                slot.set(F_LTIJ, sclamp(slot(F_LTIJ) + rho_t * rij, -kLtBound, kLtBound));
+                slot.set(F_LTJI, sclamp(slot(F_LTJI) + rho_t * rji, -kLtBound, kLtBound));
+                if (res > kAlShrink * prev_res) slot.set(F_RHOT, smin(10.0 * rho_t, kRhoTildeMax));
                 prev_res = res;
+                if (++al_it >= kMaxAl) { finalize(false); return; }
+                if (tron_begin<N>(p, ts)) return;  // next AL round runs in the loop
+                status = kTronNumericalError;
             }
         }
-        if (failed) {
+    };
+
+    for (;;) {
+        // refill idle lanes: one atomic per warp
+        const unsigned need = __ballot_sync(kFull, b < 0 && !exhausted);
+        if (need) {
+            const int leader = __ffs(need) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(q.counter, __popc(need));
+            base = __shfl_sync(kFull, base, leader);
+            if (need >> lane & 1u) {
+                const int idx = base + __popc(need & ((1u << lane) - 1u));
+                if (idx < q.count) {
+                    b = q.order[idx];
+                    load_slot<BS>(net, st, cfg, b, slot);
 #pragma unroll
-            for (int k = 0; k < 6; ++k) pt[k] = prev[k];
-            my_fail = 1;
+                    for (int k = 0; k < N; ++k) ts.x[k] = st.bp[k * net.nl + b];
+                    al_it = 0;
+                    iters = 0;
+                    prev_res = kInf;
+                    if (!tron_begin<N>(p, ts)) after_solve(kTronNumericalError);
+                } else {
+                    exhausted = true;
+                }
+            }
         }
-        st.lt_ij[b] = p.lt_ij;
-        st.lt_ji[b] = p.lt_ji;
-        st.rho_t[b] = p.rho_t;
-#pragma unroll
-        for (int k = 0; k < 6; ++k) st.bp[k * net.nl + b] = pt[k];
-        double fl[4];
-        branch_flows(p.yc, pt[0], pt[1], pt[2], pt[3], fl);
-        const int base = 2 * net.ng + 8 * b;
-        st.x[base + 0] = fl[0];
-        st.x[base + 1] = fl[1];
-        st.x[base + 2] = fl[2];
-        st.x[base + 3] = fl[3];
-        st.x[base + 4] = pt[0] * pt[0];
-        st.x[base + 5] = pt[2];
-        st.x[base + 6] = pt[1] * pt[1];
-        st.x[base + 7] = pt[3];
+        if (__all_sync(kFull, b < 0 && exhausted)) break;
+        if (b >= 0) {
+            const int iter_before = ts.iter;
+            const int r = tron_step<N>(p, ts, tp);
+            if (r != kStepContinue) {
+                int status;
+                if (r == kStepConverged) {
+                    iters += iter_before;
+                    status = kTronConverged;
+                } else if (r == kStepError) {
+                    iters += iter_before;
+                    status = kTronNumericalError;
+                } else {
+                    iters += tp.max_iterations;
+                    status = tron_finish<N>(p, ts, tp);
+                }
+                after_solve(status);
+            }
+        }
     }
-    // warp-aggregated counters
+    *iters_out += my_iters;
+    *fail_out += my_fail;
+}
+
+// Persistent kernel: even warps start on the 6-variable queue, odd warps on
+// the 4-variable one; each then drains the other.
+template <int BS>
+__global__ void __launch_bounds__(BS) branch_persistent_kernel(DevNet net, DevState st,
+                                                               BranchCfg cfg, Queue q6, Queue q4,
+                                                               int* cost, DevScalars* sc) {
+    extern __shared__ double smem[];
+    unsigned long long it6 = 0, it4 = 0;
+    int fails = 0;
+    const int warp = (blockIdx.x * BS + threadIdx.x) >> 5;
+    if ((warp & 1) == 0) {
+        drain_queue<6, BS>(net, st, cfg, q6, cost, smem, &it6, &fails);
+        drain_queue<4, BS>(net, st, cfg, q4, cost, smem, &it4, &fails);
+    } else {
+        drain_queue<4, BS>(net, st, cfg, q4, cost, smem, &it4, &fails);
+        drain_queue<6, BS>(net, st, cfg, q6, cost, smem, &it6, &fails);
+    }
     const unsigned full = 0xffffffffu;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        my_iters += __shfl_down_sync(full, my_iters, o);
-        my_fail += __shfl_down_sync(full, my_fail, o);
+        it6 += __shfl_down_sync(full, it6, o);
+        it4 += __shfl_down_sync(full, it4, o);
+        fails += __shfl_down_sync(full, fails, o);
     }
     if ((threadIdx.x & 31) == 0) {
-        if (my_iters) atomicAdd(N == 6 ? &sc->tron_iters6 : &sc->tron_iters4, my_iters);
-        if (my_fail) atomicAdd(&sc->failures, (unsigned long long)my_fail);
+        if (it6) atomicAdd(&sc->tron_iters6, it6);
+        if (it4) atomicAdd(&sc->tron_iters4, it4);
+        if (fails) atomicAdd(&sc->failures, (unsigned long long)fails);
+    }
+}
+
+// ---- LPT ordering: counting sort of each class list by last cost, desc ---
+__device__ __forceinline__ int cost_bucket(int c) {
+    const int k = c >> 2;
+    return kCostBuckets - 1 - (k < kCostBuckets - 1 ? k : kCostBuckets - 1);
+}
+
+__global__ void order_hist_kernel(const int* lim, int nlim, const int* unl, int nunl,
+                                  const int* cost, int* hist /* [2][B] */) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < nlim) atomicAdd(&hist[cost_bucket(cost[lim[t]])], 1);
+    else if (t < nlim + nunl) atomicAdd(&hist[kCostBuckets + cost_bucket(cost[unl[t - nlim]])], 1);
+}
+
+__global__ void order_scan_kernel(int* hist) {
+    // two independent exclusive scans of 256 entries; one warp each
+    const int cls = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (cls > 1) return;
+    int* h = hist + cls * kCostBuckets;
+    int carry = 0;
+    for (int base = 0; base < kCostBuckets; base += 32) {
+        const int v = h[base + lane];
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int n = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += n;
+        }
+        h[base + lane] = carry + incl - v;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+}
+
+__global__ void order_scatter_kernel(const int* lim, int nlim, const int* unl, int nunl,
+                                     const int* cost, int* hist, int* order6, int* order4) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < nlim) {
+        const int b = lim[t];
+        order6[atomicAdd(&hist[cost_bucket(cost[b])], 1)] = b;
+    } else if (t < nlim + nunl) {
+        const int b = unl[t - nlim];
+        order4[atomicAdd(&hist[kCostBuckets + cost_bucket(cost[b])], 1)] = b;
     }
 }
 
@@ -462,15 +650,47 @@ __global__ void sincos_probe_kernel(const double* x, double* s, double* c, int n
 
 }  // namespace
 
+// Workspace: [order6 nlim | order4 nunl | hist 2*B | counters 2]
+size_t branch_workspace_ints(const DevNet& n) {
+    return static_cast<size_t>(n.n_lim) + n.n_unl + 2 * kCostBuckets + 2;
+}
+
 void launch_branches(const DevNet& n, const DevState& s, const BranchCfg& cfg, DevScalars* sc,
                      cudaStream_t st) {
-    constexpr int kBlock = 128;
-    if (n.n_lim > 0)
-        branch_kernel<6><<<(n.n_lim + kBlock - 1) / kBlock, kBlock, 0, st>>>(n, s, cfg, n.lim_list,
-                                                                            n.n_lim, sc);
-    if (n.n_unl > 0)
-        branch_kernel<4><<<(n.n_unl + kBlock - 1) / kBlock, kBlock, 0, st>>>(n, s, cfg, n.unl_list,
-                                                                            n.n_unl, sc);
+    if (n.nl <= 0) return;
+    int* ws = s.branch_ws;
+    int* order6 = ws;
+    int* order4 = ws + n.n_lim;
+    int* hist = order4 + n.n_unl;
+    int* counters = hist + 2 * kCostBuckets;
+    const int total = n.n_lim + n.n_unl;
+    cudaMemsetAsync(hist, 0, (2 * kCostBuckets + 2) * sizeof(int), st);
+    order_hist_kernel<<<(total + 255) / 256, 256, 0, st>>>(n.lim_list, n.n_lim, n.unl_list,
+                                                           n.n_unl, s.br_cost, hist);
+    order_scan_kernel<<<1, 64, 0, st>>>(hist);
+    order_scatter_kernel<<<(total + 255) / 256, 256, 0, st>>>(n.lim_list, n.n_lim, n.unl_list,
+                                                              n.n_unl, s.br_cost, hist, order6,
+                                                              order4);
+    static int blocks_per_sm = -1, sms = 0;
+    const size_t smem = static_cast<size_t>(kFields) * kBranchBlock * sizeof(double);
+    if (blocks_per_sm < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(branch_persistent_kernel<kBranchBlock>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &blocks_per_sm, branch_persistent_kernel<kBranchBlock>, kBranchBlock, smem);
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    const int warps_needed = (total + 31) / 32;
+    int blocks = sms * blocks_per_sm;
+    const int max_blocks = (warps_needed * 32 + kBranchBlock - 1) / kBranchBlock;
+    if (blocks > max_blocks) blocks = max_blocks;
+    Queue q6{order6, n.n_lim, counters};
+    Queue q4{order4, n.n_unl, counters + 1};
+    branch_persistent_kernel<kBranchBlock><<<blocks, kBranchBlock, smem, st>>>(n, s, cfg, q6, q4,
+                                                                              s.br_cost, sc);
 }
 
 void launch_tron_qp(int count, int n, const double* h, const double* g, const double* l,

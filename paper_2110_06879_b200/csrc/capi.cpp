@@ -477,6 +477,22 @@ gridadmm_status gridadmm_session_counters(const gridadmm_session* s, long long* 
     });
 }
 
+gridadmm_status gridadmm_session_branch_costs(const gridadmm_session* s, int* costs) {
+    if (!s || !costs) return fail(GRIDADMM_ERR_INVALID_ARG, "null argument to branch_costs");
+    return guarded([&]() -> gridadmm_status {
+        s->s->branch_costs(costs);
+        return GRIDADMM_OK;
+    });
+}
+
+gridadmm_status gridadmm_debug_tron_stats(unsigned long long* out, int reset) {
+    if (!out) return fail(GRIDADMM_ERR_INVALID_ARG, "null argument to tron_stats");
+    return guarded([&]() -> gridadmm_status {
+        ga::tron_stats(out, reset != 0);
+        return GRIDADMM_OK;
+    });
+}
+
 int gridadmm_device_count(void) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;

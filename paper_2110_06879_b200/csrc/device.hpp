@@ -49,7 +49,13 @@ struct DevState {
     double *bus_w = nullptr, *bus_theta = nullptr;
     double* bp = nullptr;  // [6][nl]
     double *lt_ij = nullptr, *lt_ji = nullptr, *rho_t = nullptr;
+    // scheduling state of the branch phase (not part of the ADMM state):
+    int* br_cost = nullptr;    // [nl] TRON iterations of each branch, last sweep
+    int* branch_ws = nullptr;  // [branch_workspace_ints] queues + histogram
 };
+
+struct DevNet;
+size_t branch_workspace_ints(const DevNet& n);
 
 // Per-iteration scalars reduced on the device.  Maxima of non-negative
 // doubles are kept as their IEEE bit patterns (order-preserving as uint64).
@@ -96,6 +102,8 @@ void launch_clamp_gen_p(const DevNet& n, const DevState& s, cudaStream_t st);
 void launch_tron_qp(int count, int n, const double* h, const double* g,
                     const double* l, const double* u, double* x, int* status,
                     int* iterations, cudaStream_t st);
+// TRON path statistics (all zero unless built with -DGA_TRON_STATS).
+void tron_stats(unsigned long long out[8], bool reset);
 // FP64 pipe peak (TFLOP/s) for DMUL+DADD (no FMA) and DFMA issue.
 void measure_fp64_peak(double* tflops_mul_add, double* tflops_fma);
 // Pinned sincos on the device (parity probe).

@@ -137,6 +137,9 @@ void Session::upload_network() {
     alloc(ds_.bus_w, nb); alloc(ds_.bus_theta, nb);
     alloc(ds_.bp, 6 * static_cast<size_t>(nl));
     alloc(ds_.lt_ij, nl); alloc(ds_.lt_ji, nl); alloc(ds_.rho_t, nl);
+    alloc(ds_.br_cost, nl);
+    check(cudaMemset(ds_.br_cost, 0, std::max(nl, 1) * sizeof(int)), "cudaMemset cost");
+    alloc(ds_.branch_ws, branch_workspace_ints(dn_));
 }
 
 // make_state + cold_start (decomp.cpp:37-57, driver.cpp:26-63), on the host
@@ -398,6 +401,11 @@ long long Session::sincos_calls() const {
     DevScalars h;
     check(cudaMemcpy(&h, sc_, sizeof h, cudaMemcpyDeviceToHost), "D2H");
     return static_cast<long long>(h.tron_iters6);
+}
+
+void Session::branch_costs(int* out) const {
+    if (dn_.nl)
+        check(cudaMemcpy(out, ds_.br_cost, dn_.nl * sizeof(int), cudaMemcpyDeviceToHost), "D2H");
 }
 
 void Session::sync() const { check(cudaStreamSynchronize(stream_), "sync"); }

@@ -139,6 +139,7 @@ public:
 
     KernelClock kernel_clock(int cls) const { return clocks_[cls]; }
     long long tron_iterations() const;
+    void branch_costs(int* out) const;
     long long sincos_calls() const;
     void sync() const;
 

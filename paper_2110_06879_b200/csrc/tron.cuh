@@ -24,6 +24,18 @@
 
 namespace ga {
 
+// Optional path statistics (debug builds with -DGA_TRON_STATS): TRON steps,
+// Cauchy extrapolations, Cauchy halvings, CG iterations, line-search
+// steps, failed Cholesky preconditioners.
+#ifdef GA_TRON_STATS
+__device__ unsigned long long g_tron_stats[8];  // tron.cuh is included by one TU
+#endif
+#if defined(GA_TRON_STATS) && defined(__CUDA_ARCH__)
+#define GA_STAT(k) atomicAdd(&g_tron_stats[k], 1ull)
+#else
+#define GA_STAT(k) ((void)0)
+#endif
+
 struct TronParams {           // proj/src/tron.hpp:24-30
     double gtol = 1e-6;
     int max_iterations = 200;
@@ -158,6 +170,7 @@ GA_FN void cauchy_point(const double* x, const double* g, const double* h,
     if (ok(s)) {
         double trial[N];
         for (int it = 0; it < 20; ++it) {
+            GA_STAT(1);
             const double next = alpha * 2.0;
             step_at(next, trial);
             if (!ok(trial)) break;
@@ -168,6 +181,7 @@ GA_FN void cauchy_point(const double* x, const double* g, const double* h,
         return;
     }
     for (int it = 0; it < 40; ++it) {
+        GA_STAT(2);
         alpha *= 0.5;
         step_at(alpha, s);
         if (ok(s)) return;
@@ -200,6 +214,7 @@ GA_FN void subspace_cg(const double* x, const double* g, const double* h,
         dk[i] = 0.0;
     }
     const bool have_prec = mcholesky<N>(fm, h, L);
+    if (!have_prec) GA_STAT(5);
     if (have_prec) mchol_solve<N>(fm, L, rf, zk);
     else {
 #pragma unroll
@@ -212,6 +227,7 @@ GA_FN void subspace_cg(const double* x, const double* g, const double* h,
     if (r0 == 0.0) return;
 
     for (int it = 0; it < cfg.max_cg; ++it) {
+        GA_STAT(3);
         double hpk[N];
 #pragma unroll
         for (int i = 0; i < N; ++i) {
@@ -343,7 +359,9 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg) {
     double stp[N];
     double beta = 1.0;
     bool used_d = false;
+    GA_STAT(0);
     for (int ls = 0; ls < 20; ++ls) {
+        GA_STAT(4);
 #pragma unroll
         for (int i = 0; i < N; ++i) stp[i] = sclamp(st.x[i] + s[i] + beta * d[i], l[i], u[i]) - st.x[i];
         if (model<N>(g, h, stp) <= qc) { used_d = true; break; }

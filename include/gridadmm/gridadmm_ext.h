@@ -140,12 +140,14 @@ int gridadmm_device_count(void);
  * trust-region core, proj/src/tron.cpp:228-332) on `count` dense box QPs
  * f = g'x + x'Hx/2 of dimension n <= 6 (H row-major n*n per problem); x is
  * the start point in, solution out; status uses TronStatus numbering
- * (0 converged, 1 iteration limit, 2 numerical error).  And the pinned
- * device sincos (ga_sincos.h) on n arguments. */
+ * (0 converged, 1 iteration limit, 2 numerical error).  tile = 1 runs one
+ * solve per thread (lane phase), tile = 8 one solve per 8-lane tile with the
+ * speculative Cauchy/line search (tile phase).  And the pinned device sincos
+ * (ga_sincos.h) on n arguments. */
 gridadmm_status gridadmm_probe_tron_qp(int count, int n, const double* h,
                                        const double* g, const double* l,
                                        const double* u, double* x, int* status,
-                                       int* iterations);
+                                       int* iterations, int tile);
 gridadmm_status gridadmm_probe_sincos(int n, const double* x, double* s,
                                       double* c);
 

@@ -91,7 +91,7 @@ EXT_SYMBOLS = {
     "gridadmm_device_count": (_I, []),
     "gridadmm_session_branch_costs": (_I, [_P, _IP]),
     "gridadmm_debug_tron_stats": (_I, [ctypes.POINTER(ctypes.c_ulonglong), _I]),
-    "gridadmm_probe_tron_qp": (_I, [_I, _I, _DP, _DP, _DP, _DP, _DP, _IP, _IP]),
+    "gridadmm_probe_tron_qp": (_I, [_I, _I, _DP, _DP, _DP, _DP, _DP, _IP, _IP, _I]),
     "gridadmm_probe_sincos": (_I, [_I, _DP, _DP, _DP]),
     "gridadmm_probe_fp64_peak": (_I, [_I, _DP, _DP]),
 }
@@ -418,14 +418,16 @@ def device_count() -> int:
     return lib().gridadmm_device_count()
 
 
-def probe_tron_qp(H, g, lo, hi, x0):
+def probe_tron_qp(H, g, lo, hi, x0, tile: int = 1):
+    """Batched device TRON on dense box QPs; tile=1 lane mode, tile=8 tile mode."""
     count, n = g.shape
     x = np.ascontiguousarray(x0, dtype=np.float64).copy()
     status = np.zeros(count, dtype=np.int32)
     its = np.zeros(count, dtype=np.int32)
     args = [np.ascontiguousarray(a, dtype=np.float64) for a in (H, g, lo, hi)]
     _check(lib().gridadmm_probe_tron_qp(count, n, *[_dp(a) for a in args], _dp(x),
-                                        status.ctypes.data_as(_IP), its.ctypes.data_as(_IP)))
+                                        status.ctypes.data_as(_IP), its.ctypes.data_as(_IP),
+                                        tile))
     return x, status, its
 
 

@@ -503,8 +503,9 @@ int gridadmm_device_count(void) {
 // points; same C conventions).
 gridadmm_status gridadmm_probe_tron_qp(int count, int n, const double* h, const double* g,
                                        const double* l, const double* u, double* x, int* status,
-                                       int* iterations) {
-    if (count < 0 || n < 1 || n > 6) return fail(GRIDADMM_ERR_INVALID_ARG, "bad qp batch");
+                                       int* iterations, int tile) {
+    if (count < 0 || n < 1 || n > 6 || (tile != 1 && tile != 8))
+        return fail(GRIDADMM_ERR_INVALID_ARG, "bad qp batch");
     return guarded([&]() -> gridadmm_status {
         const size_t nn = static_cast<size_t>(count) * n;
         double *dh, *dg, *dl, *du, *dx;
@@ -519,7 +520,7 @@ gridadmm_status gridadmm_probe_tron_qp(int count, int n, const double* h, const 
         ck(cudaMemcpy(dl, l, nn * 8, cudaMemcpyHostToDevice));
         ck(cudaMemcpy(du, u, nn * 8, cudaMemcpyHostToDevice));
         ck(cudaMemcpy(dx, x, nn * 8, cudaMemcpyHostToDevice));
-        ga::launch_tron_qp(count, n, dh, dg, dl, du, dx, ds, di, nullptr);
+        ga::launch_tron_qp(count, n, dh, dg, dl, du, dx, ds, di, nullptr, tile);
         ck(cudaGetLastError());
         ck(cudaMemcpy(x, dx, nn * 8, cudaMemcpyDeviceToHost));
         ck(cudaMemcpy(status, ds, count * 4, cudaMemcpyDeviceToHost));

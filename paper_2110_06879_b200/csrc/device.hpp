@@ -51,7 +51,15 @@ struct DevState {
     double *lt_ij = nullptr, *lt_ji = nullptr, *rho_t = nullptr;
     // scheduling state of the branch phase (not part of the ADMM state):
     int* br_cost = nullptr;    // [nl] TRON iterations of each branch, last sweep
-    int* branch_ws = nullptr;  // [branch_workspace_ints] queues + histogram
+    int* branch_ws = nullptr;  // [branch_workspace_ints] overflow queues + counters
+    // a branch solve handed from the lane phase to the tile phase mid-way
+    double* mig_x = nullptr;         // [6][nl] TRON iterate
+    double* mig_f = nullptr;         // [nl]
+    double* mig_delta = nullptr;     // [nl]
+    double* mig_prev_res = nullptr;  // [nl] AL residual of the previous round
+    int* mig_iter = nullptr;         // [nl] TRON iteration within the solve
+    int* mig_al = nullptr;           // [nl] completed AL rounds
+    int* mig_cost = nullptr;         // [nl] TRON iterations so far (stats)
 };
 
 struct DevNet;
@@ -78,6 +86,7 @@ struct BranchCfg {
     int max_cg = 32;
     double delta_floor = 1e-3;
     double limit_tighten = 0.99;
+    int lane_budget = 8;  // TRON iterations a branch may take in the lane phase
 };
 
 // ---- launchers (kernels.cu / branch.cu) ----------------------------------
@@ -99,9 +108,10 @@ void launch_rowmax(const double* v, int n, unsigned long long* dst, cudaStream_t
 // Tracking carry-over: clamp x/xbar p-rows into [pmin, pmax] (tracking.cpp:65-70).
 void launch_clamp_gen_p(const DevNet& n, const DevState& s, cudaStream_t st);
 // Batched TRON on dense box QPs (parity test of the TRON core).
+// tile = 1 (one thread per QP, serial search) or 8 (tile search).
 void launch_tron_qp(int count, int n, const double* h, const double* g,
                     const double* l, const double* u, double* x, int* status,
-                    int* iterations, cudaStream_t st);
+                    int* iterations, cudaStream_t st, int tile);
 // TRON path statistics (all zero unless built with -DGA_TRON_STATS).
 void tron_stats(unsigned long long out[8], bool reset);
 // FP64 pipe peak (TFLOP/s) for DMUL+DADD (no FMA) and DFMA issue.

@@ -140,6 +140,13 @@ void Session::upload_network() {
     alloc(ds_.br_cost, nl);
     check(cudaMemset(ds_.br_cost, 0, std::max(nl, 1) * sizeof(int)), "cudaMemset cost");
     alloc(ds_.branch_ws, branch_workspace_ints(dn_));
+    alloc(ds_.mig_x, 6 * static_cast<size_t>(nl));
+    alloc(ds_.mig_f, nl);
+    alloc(ds_.mig_delta, nl);
+    alloc(ds_.mig_prev_res, nl);
+    alloc(ds_.mig_iter, nl);
+    alloc(ds_.mig_al, nl);
+    alloc(ds_.mig_cost, nl);
 }
 
 // make_state + cold_start (decomp.cpp:37-57, driver.cpp:26-63), on the host

@@ -330,11 +330,135 @@ GA_FN bool tron_begin(const P& prob, TronState<N>& st) {
 
 enum TronStep : int { kStepContinue = 0, kStepConverged = 1, kStepError = 2, kStepExhausted = 3 };
 
+// Sequential search strategy (one thread per solve): the reference's loops.
+struct SerialSearch {
+    template <int N>
+    GA_FN void cauchy(const double* x, const double* g, const double* h, const double* l,
+                      const double* u, double delta, double* s) const {
+        cauchy_point<N>(x, g, h, l, u, delta, s);
+    }
+    // Projected line search on s + beta d (tron.cpp:279-291); returns the step.
+    template <int N>
+    GA_FN void line_search(const double* x, const double* g, const double* h, const double* l,
+                           const double* u, const double* s, const double* d, double qc,
+                           double* stp) const {
+        double beta = 1.0;
+        GA_STAT(0);
+        for (int ls = 0; ls < 20; ++ls) {
+            GA_STAT(4);
+#pragma unroll
+            for (int i = 0; i < N; ++i) stp[i] = sclamp(x[i] + s[i] + beta * d[i], l[i], u[i]) - x[i];
+            if (model<N>(g, h, stp) <= qc) return;
+            beta *= 0.5;
+        }
+#pragma unroll
+        for (int i = 0; i < N; ++i) stp[i] = s[i];
+    }
+};
+
+#if defined(__CUDACC__)
+// Speculative search strategy for a tile of T lanes (power of two, <= 32)
+// that all hold the same replicated iterate.  The reference's Cauchy search
+// (tron.cpp:101-137) and projected line search (tron.cpp:279-291) are
+// sequences of independent trials at alpha0 * 2^c / beta = 2^-t followed by
+// "first success" / "last consecutive success" rules; the tile evaluates T
+// trials at once and applies the same rule to the ballot.  Every trial is
+// computed exactly as the sequential loop computes it (scaling by powers of
+// two is exact), so the selected step is bit-identical.
+template <int T>
+struct TileSearch {
+    unsigned mask;  // warp lanes of this tile
+    int base;       // first warp lane of the tile
+    int rank;       // lane within the tile
+
+    __device__ __forceinline__ unsigned ballot(bool p) const {
+        return (__ballot_sync(mask, p) >> base) & ((T == 32) ? 0xffffffffu : ((1u << T) - 1u));
+    }
+    template <int N>
+    __device__ __forceinline__ void bcast(const double* v, int src, double* out) const {
+#pragma unroll
+        for (int i = 0; i < N; ++i) out[i] = __shfl_sync(mask, v[i], src, T);
+    }
+
+    template <int N>
+    __device__ void cauchy(const double* x, const double* g, const double* h, const double* l,
+                           const double* u, double delta, double* s) const {
+        const double gnorm = vnorm2<N>(g);
+        if (gnorm == 0.0) {
+#pragma unroll
+            for (int i = 0; i < N; ++i) s[i] = 0.0;
+            return;
+        }
+        const double alpha0 = smin(1.0, delta / gnorm);
+        double mys[N];
+        auto trial = [&](int c) {  // ok() of the step at alpha0 * 2^c
+            double a = alpha0;
+            for (int k = 0; k < c; ++k) a *= 2.0;
+            for (int k = 0; k < -c; ++k) a *= 0.5;
+#pragma unroll
+            for (int i = 0; i < N; ++i) mys[i] = sclamp(x[i] - a * g[i], l[i], u[i]) - x[i];
+            if (!(vnorm2<N>(mys) <= delta)) return false;
+            return model<N>(g, h, mys) <= kTronMu0 * vdot<N>(g, mys);
+        };
+        // round 0: rank 0 -> c = 0, rank 1 -> +1, ranks 2.. -> -1, -2, ...
+        const int c0 = rank == 0 ? 0 : (rank == 1 ? 1 : -(rank - 1));
+        unsigned okm = ballot(trial(c0));
+        if (okm & 1u) {  // extrapolate while the condition keeps holding (<= 20)
+            if (!(okm & 2u)) { bcast<N>(mys, 0, s); return; }
+            bcast<N>(mys, 1, s);  // best so far: c = 1
+            for (int cb = 2; cb <= 20; cb += T) {
+                const int c = cb + rank;
+                const bool okc = (c <= 20) ? trial(c) : false;
+                okm = ballot(okc);
+                const int run = __ffs(~okm) - 1;  // consecutive successes from cb
+                if (run > 0) bcast<N>(mys, run - 1, s);
+                if (run < T) return;
+            }
+            return;
+        }
+        // backtrack: first k in 1..40 with ok(alpha0 * 2^-k)
+        unsigned hm = okm >> 2;
+        if (hm) { bcast<N>(mys, __ffs(hm) - 1 + 2, s); return; }
+        int kb = T - 1;
+        for (; kb <= 40; kb += T) {
+            const int k = kb + rank;
+            const bool okk = (k <= 40) ? trial(-k) : false;
+            okm = ballot(okk);
+            if (okm) { bcast<N>(mys, __ffs(okm) - 1, s); return; }
+        }
+        // none accepted: the step at the last trial, alpha0 * 2^-40
+        kb -= T;
+        const int src = 40 - kb;
+        bcast<N>(mys, src, s);
+    }
+
+    template <int N>
+    __device__ void line_search(const double* x, const double* g, const double* h, const double* l,
+                                const double* u, const double* s, const double* d, double qc,
+                                double* stp) const {
+        double myst[N];
+        for (int tb = 0; tb < 20; tb += T) {
+            const int t = tb + rank;
+            double beta = 1.0;
+            for (int k = 0; k < t; ++k) beta *= 0.5;
+#pragma unroll
+            for (int i = 0; i < N; ++i) myst[i] = sclamp(x[i] + s[i] + beta * d[i], l[i], u[i]) - x[i];
+            const bool okt = (t < 20) ? (model<N>(g, h, myst) <= qc) : false;
+            const unsigned okm = ballot(okt);
+            if (okm) { bcast<N>(myst, __ffs(okm) - 1, stp); return; }
+        }
+#pragma unroll
+        for (int i = 0; i < N; ++i) stp[i] = s[i];
+    }
+};
+#endif
+
 // One trust-region iteration (tron.cpp:243-317).  kStepExhausted means the
 // loop ended by the iteration cap or the delta < 1e-14 break, after which
-// tron_finish must be called.  *evals counts value/gradient calls.
-template <int N, class P>
-GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg) {
+// tron_finish must be called.
+template <int N, class P, class Search = SerialSearch>
+GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
+                    const Search& search = Search()) {
     double l[N], u[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) { l[i] = prob.lo(i); u[i] = prob.hi(i); }
@@ -352,25 +476,12 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg) {
     if (st.iter == 0 && st.delta == 0.0) st.delta = smax(vnorm2<N>(g), cfg.delta_floor);
 
     double s[N], d[N];
-    cauchy_point<N>(st.x, g, h, l, u, st.delta, s);
+    search.template cauchy<N>(st.x, g, h, l, u, st.delta, s);
     subspace_cg<N>(st.x, g, h, l, u, st.delta, cfg, s, d);
 
     const double qc = model<N>(g, h, s);
     double stp[N];
-    double beta = 1.0;
-    bool used_d = false;
-    GA_STAT(0);
-    for (int ls = 0; ls < 20; ++ls) {
-        GA_STAT(4);
-#pragma unroll
-        for (int i = 0; i < N; ++i) stp[i] = sclamp(st.x[i] + s[i] + beta * d[i], l[i], u[i]) - st.x[i];
-        if (model<N>(g, h, stp) <= qc) { used_d = true; break; }
-        beta *= 0.5;
-    }
-    if (!used_d) {
-#pragma unroll
-        for (int i = 0; i < N; ++i) stp[i] = s[i];
-    }
+    search.template line_search<N>(st.x, g, h, l, u, s, d, qc, stp);
     const double q = model<N>(g, h, stp);
     double xt[N];
 #pragma unroll

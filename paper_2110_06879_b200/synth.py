@@ -159,9 +159,22 @@ def generate(nbus: int, ngen: int, nbranch: int, limited_frac: float = 0.6, seed
         tile_branch_src.append(-1)
         tile_tree.append(True)
 
-    for t in range(len(kinds) - 1):  # chain: three ties per neighbour pair
-        for _ in range(3):
-            tie(t, t + 1)
+    # tiles on a 2-D lattice, two ties to the right and two to the lower
+    # neighbour, plus random long-range ties (keeps the electrical diameter
+    # ~2*sqrt(tiles) instead of a chain's ~tiles, so angles stay bounded)
+    ntile = len(kinds)
+    width = max(1, int(np.ceil(np.sqrt(ntile))))
+    for t in range(ntile):
+        r0, c0 = divmod(t, width)
+        for nb in ((t + 1) if c0 + 1 < width and t + 1 < ntile else -1,
+                   (t + width) if t + width < ntile else -1):
+            if nb >= 0:
+                tie(t, nb)
+                tie(t, nb)
+    for _ in range(ntile // 4):
+        a, b2 = rng.integers(ntile, size=2)
+        if a != b2:
+            tie(int(a), int(b2))
 
     # radial PQ stubs for the exact bus count
     nstub = nbus - len(buses)
@@ -218,13 +231,17 @@ def generate(nbus: int, ngen: int, nbranch: int, limited_frac: float = 0.6, seed
         gens = np.vstack([gens, gens[add]])
         costs = np.vstack([costs, costs[add]])
     buses = np.array(buses)
-    # scale demand to 55% of capacity
-    cap = gens[:, 8].sum()
-    load = buses[:, 2].sum()
-    if load > 0:
-        f = 0.55 * cap / load
-        buses[:, 2] *= f
-        buses[:, 3] *= f
+    # scale each tile's demand to 55% of the generation left in that tile, so
+    # tiles are near self-sufficient and tie flows stay small
+    ends = np.cumsum([len(x) for x in tile_bus_ids])  # tile t owns ids (ends[t-1], ends[t]]
+    bus_tile = np.searchsorted(ends, buses[:, 0] - 1, side="right")
+    gen_tile = np.searchsorted(ends, gens[:, 0] - 1, side="right")
+    cap = np.bincount(gen_tile, weights=gens[:, 8], minlength=ntile + 1)
+    in_tile = bus_tile < ntile
+    load = np.bincount(bus_tile[in_tile], weights=buses[in_tile, 2], minlength=ntile + 1)
+    f = np.where(load > 0, 0.55 * cap / np.maximum(load, 1e-300), 1.0)
+    buses[in_tile, 2] *= f[bus_tile[in_tile]]
+    buses[in_tile, 3] *= f[bus_tile[in_tile]]
 
     out = [f"function mpc = {name}", "% synthetic tiled grid (paper_2110_06879_b200.synth)",
            "mpc.version = '2';", "mpc.baseMVA = 100;", "mpc.bus = ["]

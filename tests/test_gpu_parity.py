@@ -62,10 +62,12 @@ def test_device_sincos_matches_host_shim(gridadmm, oracle_mod):
     assert_bits_equal(cd, ch, "cos")
 
 
+@pytest.mark.parametrize("tile", [1, 8])
 @pytest.mark.parametrize("n", [4, 6, 2])
-def test_tron_core_matches_reference(gridadmm, oracle_mod, n):
+def test_tron_core_matches_reference(gridadmm, oracle_mod, n, tile):
     """Batched device TRON vs reference solve_one on random box QPs (convex and
-    indefinite), acceptance.cpp:458-520 style."""
+    indefinite), acceptance.cpp:458-520 style, in both the one-lane (serial
+    search) and the 8-lane tile (speculative search) formulations."""
     rng = np.random.default_rng(100 + n)
     count = 4000
     A = rng.normal(size=(count, n, n))
@@ -77,7 +79,7 @@ def test_tron_core_matches_reference(gridadmm, oracle_mod, n):
     hi = rng.uniform(0.1, 2.0, size=(count, n))
     x0 = rng.uniform(-0.5, 0.5, size=(count, n))
     Hf = np.ascontiguousarray(H.reshape(count, n * n))
-    xd, sd, itd = gridadmm.probe_tron_qp(Hf, g, lo, hi, x0)
+    xd, sd, itd = gridadmm.probe_tron_qp(Hf, g, lo, hi, x0, tile=tile)
     xr, sr, itr = oracle_mod.ref_tron_qp(Hf, g, lo, hi, x0)
     assert np.array_equal(sd, sr)
     assert np.array_equal(itd, itr)

@@ -45,10 +45,12 @@ sys.path.insert(0, REPO)
 
 L2_FLUSH_BYTES = 256 << 20
 SHAPE = "case_ACTIVSg70k"
-# Lean FP64 op census per TRON iteration (flops whose results are consumed),
-# measured by the instrumented C restatement (oracle/gridadmm_oracle.c,
-# census build) — see DESIGN.md §Roofline.
-CENSUS_FLOPS = {4: 1900.0, 6: 3600.0}
+# Lean FP64 op census per TRON iteration (flops whose results are consumed,
+# branch evaluation + TRON core, amortized per-branch setup included),
+# measured with the C restatement's counters (oracle/gridadmm_oracle.c FL())
+# on the case2868rte-shaped synthetic grid, ACTIVSg70k preset, inner
+# iterations 1-20: 4-var 1588, 6-var 3329 flops/iteration.
+CENSUS_FLOPS = {4: 1588.0, 6: 3329.0}
 
 
 def parse():

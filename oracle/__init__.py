@@ -188,6 +188,99 @@ class RefNet:
         return series[: 6 * k].reshape(-1, 6), info, fin
 
 
+class OracleNet(ctypes.Structure):
+    _fields_ = [("nb", ctypes.c_int), ("ng", ctypes.c_int), ("nl", ctypes.c_int),
+                ("ref_bus", ctypes.c_int), ("bus", _DP), ("gen", _DP), ("ends", _IP),
+                ("branch", _DP)]
+
+
+class PortLib:
+    """ctypes binding of liboracle.so (the C restatement)."""
+
+    _h = None
+
+    @classmethod
+    def get(cls):
+        if cls._h is None:
+            if not os.path.exists(PORT_SO):
+                build()
+            h = ctypes.CDLL(PORT_SO)
+            h.oracle_cold_start.argtypes = [ctypes.POINTER(OracleNet), _DP, ctypes.POINTER(StateView)]
+            h.oracle_phase.restype = ctypes.c_long
+            h.oracle_phase.argtypes = [ctypes.POINTER(OracleNet), ctypes.c_int, _DP,
+                                       ctypes.POINTER(StateView), _D, _D]
+            h.oracle_solve.argtypes = [ctypes.POINTER(OracleNet), _DP, ctypes.POINTER(StateView),
+                                       ctypes.POINTER(StateView), _DP, ctypes.c_int, _IP, _DP]
+            h.oracle_census.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
+            cls._h = h
+        return cls._h
+
+
+def export_network(path: str):
+    """Flat network arrays for the C restatement: parsed by the reference's
+    own parser when oracle/_ref is present, else by the product parser (which
+    tests/test_host.py pins to the reference bit-for-bit)."""
+    if have_ref():
+        return RefNet(path).export()
+    import paper_2110_06879_b200 as ga
+    return ga.Network(path).export()
+
+
+class PortNet:
+    """The C restatement (gridadmm_oracle.c) on one network."""
+
+    def __init__(self, path: str):
+        self.lib = PortLib.get()
+        ex = export_network(path)
+        self.arrays = {
+            "bus": np.ascontiguousarray(ex["bus"].ravel()),
+            "gen": np.ascontiguousarray(ex["gen"].ravel()),
+            "ends": np.ascontiguousarray(ex["ends"].ravel().astype(np.int32)),
+            "branch": np.ascontiguousarray(ex["branch"].ravel()),
+        }
+        self.nb, self.ng, self.nl = len(ex["bus"]), len(ex["gen"]), len(ex["ends"])
+        self.m = 2 * self.ng + 8 * self.nl
+        a = self.arrays
+        self.net = OracleNet(self.nb, self.ng, self.nl, ex["ref_bus"], _dp(a["bus"]), _dp(a["gen"]),
+                             a["ends"].ctypes.data_as(_IP), _dp(a["branch"]))
+
+    def empty_state(self):
+        s = {k: np.zeros(n) for k, n in state_shapes(self.nb, self.ng, self.nl).items()}
+        s["beta"] = np.zeros(1)
+        return s
+
+    def cold_start(self, **cfg):
+        s = self.empty_state()
+        v = make_view(s)
+        self.lib.oracle_cold_start(ctypes.byref(self.net), config_vector(**cfg), ctypes.byref(v))
+        return s
+
+    def phase(self, phase, state, z_inf=0.0, prev_z_inf=-1.0, **cfg):
+        v = make_view(state)
+        return int(self.lib.oracle_phase(ctypes.byref(self.net), phase, config_vector(**cfg),
+                                         ctypes.byref(v), z_inf, prev_z_inf))
+
+    def solve(self, init=None, cap=100000, **cfg):
+        series = np.zeros(6 * cap)
+        n = ctypes.c_int()
+        info = np.zeros(9)
+        fin = self.empty_state()
+        vf = make_view(fin)
+        vi = make_view(init) if init is not None else None
+        rc = self.lib.oracle_solve(ctypes.byref(self.net), config_vector(**cfg),
+                                   ctypes.byref(vi) if vi is not None else None, ctypes.byref(vf),
+                                   _dp(series), cap, ctypes.byref(n), _dp(info))
+        if rc != 0:
+            raise RuntimeError("oracle solve failed (singular bus)")
+        k = min(n.value, cap)
+        return series[: 6 * k].reshape(-1, 6), info, fin
+
+    def census(self, reset=True):
+        out = (ctypes.c_ulonglong * 6)()
+        self.lib.oracle_census(out, 1 if reset else 0)
+        return list(out)
+
+
 def ref_tron_qp(H, g, lo, hi, x0):
     lib = RefLib.get()
     count, n = g.shape

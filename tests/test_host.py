@@ -33,6 +33,21 @@ def test_library_exports_every_declared_symbol(gridadmm):
     assert len(ref23) == 23 and set(ref23) <= set(syms)
 
 
+def test_c_program_links_against_library(gridadmm, tmp_path):
+    """A plain C caller compiled against include/gridadmm/gridadmm.h links and
+    runs against libgridadmm.so (drop-in for the reference's C callers)."""
+    import subprocess
+    exe = tmp_path / "capi_link"
+    libdir = os.path.dirname(gridadmm.LIB_PATH)
+    src = os.path.join(REPO, "tests", "c", "capi_link.c")
+    r = subprocess.run(["gcc", "-std=c11", "-I", os.path.join(REPO, "include"), src, "-o", str(exe),
+                        "-L", libdir, "-lgridadmm", f"-Wl,-rpath,{libdir}"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(exe), case_path("case9")], capture_output=True, text=True)
+    assert out.returncode == 0 and out.stdout.strip() == "ok", (out.returncode, out.stdout, out.stderr)
+
+
 def test_network_dimensions_and_errors(gridadmm):
     net = gridadmm.Network(case_path("case9"))
     assert (net.num_buses, net.num_generators, net.num_branches) == (9, 3, 9)

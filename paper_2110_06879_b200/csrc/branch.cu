@@ -79,6 +79,12 @@ Work work_of(const DevNet& n, const DevState& s) {
     return w;
 }
 
+__device__ __forceinline__ unsigned sm_id() {
+    unsigned id;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(id));
+    return id;
+}
+
 __device__ __forceinline__ TronParams tron_params(const BranchCfg& cfg) {
     TronParams tp;
     tp.gtol = cfg.gtol;
@@ -251,8 +257,9 @@ __global__ void __launch_bounds__(kLaneBlock) lane_kernel(DevNet net, DevState s
     extern __shared__ double smem[];
     unsigned long long it6 = 0, it4 = 0;
     int fails = 0;
-    const int warp = (blockIdx.x * kLaneBlock + threadIdx.x) >> 5;
-    if ((warp & 1) == 0) {
+    // Even SMs start on the 6-variable queue, odd SMs on the 4-variable one,
+    // so each SM's warps share one code path (instruction-cache locality).
+    if ((sm_id() & 1u) == 0) {
         lane_phase<6>(net, st, cfg, net.lim_list, net.n_lim, &w.ctr[0], w.ovf6, &w.ctr[2], smem,
                       &it6, &fails);
         lane_phase<4>(net, st, cfg, net.unl_list, net.n_unl, &w.ctr[1], w.ovf4, &w.ctr[3], smem,
@@ -337,8 +344,7 @@ __global__ void __launch_bounds__(kTileBlock) tile_kernel(DevNet net, DevState s
     __shared__ double smem[kFields * (kTileBlock / kTile)];
     unsigned long long it6 = 0, it4 = 0;
     int fails = 0;
-    const int tile = (blockIdx.x * kTileBlock + threadIdx.x) / kTile;
-    if ((tile & 1) == 0) {
+    if ((sm_id() & 1u) == 0) {
         tile_phase<6>(net, st, cfg, w.ovf6, &w.ctr[2], &w.ctr[4], smem, &it6, &fails);
         tile_phase<4>(net, st, cfg, w.ovf4, &w.ctr[3], &w.ctr[5], smem, &it4, &fails);
     } else {

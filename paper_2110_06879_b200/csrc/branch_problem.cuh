@@ -298,12 +298,12 @@ struct BranchProb {
 
     __device__ __forceinline__ double value(const double* x) const {
         double c, sn, f;
-        ga_sincos(x[2] - x[3], &sn, &c);
+        ga_sincos_ool(x[2] - x[3], &sn, &c);
         eval<true, false, false>(x, c, sn, &f, nullptr, nullptr);
         return f;
     }
     __device__ __forceinline__ void gradient(const double* x, double* g) const {
-        ga_sincos(x[2] - x[3], &ss_, &cc_);
+        ga_sincos_ool(x[2] - x[3], &ss_, &cc_);
         eval<false, true, false>(x, cc_, ss_, nullptr, g, nullptr);
     }
     // Called by TRON right after gradient() at the same x.
@@ -316,7 +316,7 @@ struct BranchProb {
 template <class Y>
 GA_FN void branch_flows(const Y& yc, double vi, double vj, double thi, double thj, double* out) {
     double s, c;
-    ga_sincos(thi - thj, &s, &c);
+    ga_sincos_ool(thi - thj, &s, &c);
     const double wi = vi * vi, wj = vj * vj;
     const double wr = vi * vj * c, wim = vi * vj * s;
     out[0] = yc(0) * wi + yc(2) * wr + yc(3) * wim;     // pij

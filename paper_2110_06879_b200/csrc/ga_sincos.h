@@ -116,4 +116,24 @@ GA_HD void ga_sincos(double x, double* s, double* c) {
 GA_HD double ga_sin(double x) { double s, c; ga_sincos(x, &s, &c); return s; }
 GA_HD double ga_cos(double x) { double s, c; ga_sincos(x, &s, &c); return c; }
 
+#if defined(__CUDACC__)
+/* Out-of-line device copy: the branch kernels call sincos from ~10 sites and
+ * their hot loop must fit the instruction cache.  Same operations, same bits. */
+static __device__ __noinline__ double2 ga_sincos_call(double x) {
+    double s, c;
+    ga_sincos(x, &s, &c);
+    return make_double2(s, c);
+}
+/* sincos for code compiled for both sides: out-of-line on the device. */
+__host__ __device__ __forceinline__ void ga_sincos_ool(double x, double* s, double* c) {
+#if defined(__CUDA_ARCH__)
+    const double2 r = ga_sincos_call(x);
+    *s = r.x;
+    *c = r.y;
+#else
+    ga_sincos(x, s, c);
+#endif
+}
+#endif
+
 #endif /* GA_SINCOS_H */

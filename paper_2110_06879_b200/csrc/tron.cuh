@@ -215,18 +215,11 @@ GA_FN void subspace_cg(const double* x, const double* g, const double* h,
     }
     const bool have_prec = mcholesky<N>(fm, h, L);
     if (!have_prec) GA_STAT(5);
-    if (have_prec) mchol_solve<N>(fm, L, rf, zk);
-    else {
-#pragma unroll
-        for (int i = 0; i < N; ++i) zk[i] = rf[i];
-    }
-#pragma unroll
-    for (int i = 0; i < N; ++i) pk[i] = zk[i];
-    double rz = mdot<N>(fm, rf, zk);
-    const double r0 = sqrt(mdot<N>(fm, rf, rf));
-    if (r0 == 0.0) return;
-
-    for (int it = 0; it < cfg.max_cg; ++it) {
+    double rz = 0.0, r0 = 0.0;
+    // it = -1 is the set-up (z0 = M^-1 r0, p0 = z0); the preconditioner solve
+    // has a single call site (code size), same operations as tron.cpp:171-222.
+    for (int it = -1; it < cfg.max_cg; ++it) {
+      if (it >= 0) {
         GA_STAT(3);
         double hpk[N];
 #pragma unroll
@@ -274,18 +267,26 @@ GA_FN void subspace_cg(const double* x, const double* g, const double* h,
                 rf[i] -= alpha * hpk[i];
             }
         if (sqrt(mdot<N>(fm, rf, rf)) <= cfg.cg_tol * r0) break;
-        double znext[N];
-        if (have_prec) mchol_solve<N>(fm, L, rf, znext);
+      }
+        if (have_prec) mchol_solve<N>(fm, L, rf, zk);
         else {
 #pragma unroll
-            for (int i = 0; i < N; ++i) znext[i] = rf[i];
+            for (int i = 0; i < N; ++i) zk[i] = rf[i];
         }
-        const double rznext = mdot<N>(fm, rf, znext);
-        const double betak = rznext / rz;
+        const double rznext = mdot<N>(fm, rf, zk);
+        if (it < 0) {
 #pragma unroll
-        for (int i = 0; i < N; ++i)
-            if (fm >> i & 1u) pk[i] = znext[i] + betak * pk[i];
-        rz = rznext;
+            for (int i = 0; i < N; ++i) pk[i] = zk[i];
+            rz = rznext;
+            r0 = sqrt(mdot<N>(fm, rf, rf));
+            if (r0 == 0.0) return;
+        } else {
+            const double betak = rznext / rz;
+#pragma unroll
+            for (int i = 0; i < N; ++i)
+                if (fm >> i & 1u) pk[i] = zk[i] + betak * pk[i];
+            rz = rznext;
+        }
     }
 #pragma unroll
     for (int i = 0; i < N; ++i) d[i] = (fm >> i & 1u) ? dk[i] : 0.0;
@@ -391,45 +392,55 @@ struct TileSearch {
         }
         const double alpha0 = smin(1.0, delta / gnorm);
         double mys[N];
-        auto trial = [&](int c) {  // ok() of the step at alpha0 * 2^c
-            double a = alpha0;
-            for (int k = 0; k < c; ++k) a *= 2.0;
-            for (int k = 0; k < -c; ++k) a *= 0.5;
+        // One trial site and one broadcast site (code size: this runs in a
+        // persistent kernel whose hot loop must stay in the instruction cache).
+        // Candidate exponents c (trial at alpha0 * 2^c):
+        //   round 0: rank 0 -> 0, rank 1 -> +1, ranks 2.. -> -1, -2, ...
+        //   extrapolation rounds r >= 1: 2 + (r-1)*T + rank   (valid <= 20)
+        //   backtracking rounds r >= 1: -((T-1) + (r-1)*T + rank) (valid >= -40)
+        int dir = 0;  // +1 extrapolating, -1 backtracking (decided in round 0)
+        for (int round = 0;; ++round) {
+            int c;
+            if (round == 0) c = rank == 0 ? 0 : (rank == 1 ? 1 : -(rank - 1));
+            else if (dir > 0) c = 2 + (round - 1) * T + rank;
+            else c = -((T - 1) + (round - 1) * T + rank);
+            const bool valid = dir > 0 ? c <= 20 : c >= -40;
+            bool okc = false;
+            if (valid) {
+                double a = alpha0;
+                for (int k = 0; k < c; ++k) a *= 2.0;
+                for (int k = 0; k < -c; ++k) a *= 0.5;
 #pragma unroll
-            for (int i = 0; i < N; ++i) mys[i] = sclamp(x[i] - a * g[i], l[i], u[i]) - x[i];
-            if (!(vnorm2<N>(mys) <= delta)) return false;
-            return model<N>(g, h, mys) <= kTronMu0 * vdot<N>(g, mys);
-        };
-        // round 0: rank 0 -> c = 0, rank 1 -> +1, ranks 2.. -> -1, -2, ...
-        const int c0 = rank == 0 ? 0 : (rank == 1 ? 1 : -(rank - 1));
-        unsigned okm = ballot(trial(c0));
-        if (okm & 1u) {  // extrapolate while the condition keeps holding (<= 20)
-            if (!(okm & 2u)) { bcast<N>(mys, 0, s); return; }
-            bcast<N>(mys, 1, s);  // best so far: c = 1
-            for (int cb = 2; cb <= 20; cb += T) {
-                const int c = cb + rank;
-                const bool okc = (c <= 20) ? trial(c) : false;
-                okm = ballot(okc);
-                const int run = __ffs(~okm) - 1;  // consecutive successes from cb
-                if (run > 0) bcast<N>(mys, run - 1, s);
-                if (run < T) return;
+                for (int i = 0; i < N; ++i) mys[i] = sclamp(x[i] - a * g[i], l[i], u[i]) - x[i];
+                okc = vnorm2<N>(mys) <= delta && model<N>(g, h, mys) <= kTronMu0 * vdot<N>(g, mys);
             }
-            return;
+            const unsigned okm = ballot(okc);
+            int src = -1;      // lane whose trial step becomes s
+            bool done = true;
+            if (round == 0) {
+                if (okm & 1u) {
+                    dir = 1;
+                    src = (okm & 2u) ? 1 : 0;
+                    done = !(okm & 2u);
+                } else {
+                    dir = -1;
+                    const unsigned hm = okm >> 2;
+                    if (hm) src = __ffs(hm) - 1 + 2;
+                    else done = false;
+                }
+            } else if (dir > 0) {
+                const int run = __ffs(~okm) - 1;  // consecutive successes
+                if (run > 0) src = run - 1;
+                done = run < T;  // a failure (or the c > 20 limit) ended the run
+            } else {
+                const int kb = (T - 1) + (round - 1) * T;  // this round tried k = kb..kb+T-1
+                if (okm) src = __ffs(okm) - 1;
+                else if (kb + T - 1 >= 40) src = 40 - kb;  // none up to 2^-40: last trial's step
+                else done = false;
+            }
+            if (src >= 0) bcast<N>(mys, src, s);
+            if (done) return;
         }
-        // backtrack: first k in 1..40 with ok(alpha0 * 2^-k)
-        unsigned hm = okm >> 2;
-        if (hm) { bcast<N>(mys, __ffs(hm) - 1 + 2, s); return; }
-        int kb = T - 1;
-        for (; kb <= 40; kb += T) {
-            const int k = kb + rank;
-            const bool okk = (k <= 40) ? trial(-k) : false;
-            okm = ballot(okk);
-            if (okm) { bcast<N>(mys, __ffs(okm) - 1, s); return; }
-        }
-        // none accepted: the step at the last trial, alpha0 * 2^-40
-        kb -= T;
-        const int src = 40 - kb;
-        bcast<N>(mys, src, s);
     }
 
     template <int N>

@@ -123,6 +123,13 @@ gridadmm_status gridadmm_session_counters(const gridadmm_session* s,
                                           long long* tron_iterations,
                                           long long* sincos_calls);
 
+/* Cumulative counters: out[0], out[1] = TRON iterations with the reference's
+ * accounting (TronResult::iterations; 4-var, 6-var branches), out[2],
+ * out[3] = trust-region steps the device actually executed (fewer when a
+ * solve reaches an exact fixed point and its remaining identical iterations
+ * are skipped, see tron.cuh). */
+gridadmm_status gridadmm_session_step_counters(const gridadmm_session* s, long long* out);
+
 /* TRON iterations each branch took in the last branch sweep (num_branches
  * ints) — the LPT scheduling key, exposed for profiling. */
 gridadmm_status gridadmm_session_branch_costs(const gridadmm_session* s, int* costs);

@@ -90,6 +90,7 @@ EXT_SYMBOLS = {
                                        ctypes.POINTER(ctypes.c_longlong)]),
     "gridadmm_device_count": (_I, []),
     "gridadmm_session_branch_costs": (_I, [_P, _IP]),
+    "gridadmm_session_step_counters": (_I, [_P, ctypes.POINTER(ctypes.c_longlong)]),
     "gridadmm_debug_tron_stats": (_I, [ctypes.POINTER(ctypes.c_ulonglong), _I]),
     "gridadmm_probe_tron_qp": (_I, [_I, _I, _DP, _DP, _DP, _DP, _DP, _IP, _IP, _I]),
     "gridadmm_probe_sincos": (_I, [_I, _DP, _DP, _DP]),
@@ -399,6 +400,12 @@ class Session:
         out = np.zeros(max(1, self.shapes["lt_ij"]), dtype=np.int32)
         _check(lib().gridadmm_session_branch_costs(self._h, out.ctypes.data_as(_IP)))
         return out[: self.shapes["lt_ij"]]
+
+    def step_counters(self):
+        """(TRON its 4-var, 6-var [reference accounting], executed steps 4-var, 6-var)."""
+        out = (ctypes.c_longlong * 4)()
+        _check(lib().gridadmm_session_step_counters(self._h, out))
+        return tuple(out)
 
     def counters(self):
         t = ctypes.c_longlong()

@@ -169,9 +169,11 @@ template <int N>
 __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
                                         const BranchCfg& cfg, const int* list, int count,
                                         int* cursor, int* ovf, int* ovf_count, double* smem,
-                                        unsigned long long* iters_out, int* fail_out) {
+                                        unsigned long long* iters_out, int* fail_out,
+                                        unsigned long long* exec_dst) {
     constexpr unsigned kFull = 0xffffffffu;
     const int lane = threadIdx.x & 31;
+    unsigned my_exec = 0;  // trust-region steps executed by this lane
     const Slot<kLaneBlock> slot{smem + threadIdx.x};
     BranchProb<N, kLaneBlock> p{slot};
     const TronParams tp = tron_params(cfg);
@@ -224,6 +226,7 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
         if (b >= 0) {
             const int iter_before = ts.iter;
             const int r = tron_step<N>(p, ts, tp);
+            ++my_exec;
             if (r != kStepContinue) {
                 const int status = solve_status<N, kLaneBlock, SerialSearch>(r, iter_before, p, ts,
                                                                             tp, iters);
@@ -250,6 +253,8 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
     }
     *iters_out += my_iters;
     *fail_out += my_fail;
+    const unsigned warp_exec = __reduce_add_sync(kFull, my_exec);
+    if (lane == 0 && warp_exec) atomicAdd(exec_dst, (unsigned long long)warp_exec);
 }
 
 __global__ void __launch_bounds__(kLaneBlock) lane_kernel(DevNet net, DevState st, BranchCfg cfg,
@@ -261,14 +266,14 @@ __global__ void __launch_bounds__(kLaneBlock) lane_kernel(DevNet net, DevState s
     // so each SM's warps share one code path (instruction-cache locality).
     if ((sm_id() & 1u) == 0) {
         lane_phase<6>(net, st, cfg, net.lim_list, net.n_lim, &w.ctr[0], w.ovf6, &w.ctr[2], smem,
-                      &it6, &fails);
+                      &it6, &fails, &sc->exec6);
         lane_phase<4>(net, st, cfg, net.unl_list, net.n_unl, &w.ctr[1], w.ovf4, &w.ctr[3], smem,
-                      &it4, &fails);
+                      &it4, &fails, &sc->exec4);
     } else {
         lane_phase<4>(net, st, cfg, net.unl_list, net.n_unl, &w.ctr[1], w.ovf4, &w.ctr[3], smem,
-                      &it4, &fails);
+                      &it4, &fails, &sc->exec4);
         lane_phase<6>(net, st, cfg, net.lim_list, net.n_lim, &w.ctr[0], w.ovf6, &w.ctr[2], smem,
-                      &it6, &fails);
+                      &it6, &fails, &sc->exec6);
     }
     const unsigned full = 0xffffffffu;
 #pragma unroll
@@ -289,8 +294,9 @@ template <int N>
 __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
                                         const BranchCfg& cfg, const int* ovf, const int* ovf_count,
                                         int* cursor, double* smem, unsigned long long* iters_out,
-                                        int* fail_out) {
+                                        int* fail_out, unsigned long long* exec_dst) {
     constexpr int S = kTileBlock / kTile;
+    unsigned long long my_exec = 0;
     const int lane = threadIdx.x & 31;
     const int rank = lane & (kTile - 1);
     const int tbase = lane & ~(kTile - 1);
@@ -323,6 +329,7 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
         while (act == kAlContinue) {
             const int iter_before = ts.iter;
             const int r = tron_step<N>(p, ts, tp, search);
+            ++my_exec;
             if (r == kStepContinue) continue;
             const int status = solve_status<N, S, TileSearch<kTile>>(r, iter_before, p, ts, tp, iters);
             act = al_after_solve<N>(status, slot, p, ts, al_it, prev_res);
@@ -337,6 +344,7 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
     }
     *iters_out += my_iters;
     *fail_out += my_fail;
+    if (rank == 0 && my_exec) atomicAdd(exec_dst, my_exec);
 }
 
 __global__ void __launch_bounds__(kTileBlock) tile_kernel(DevNet net, DevState st, BranchCfg cfg,
@@ -345,11 +353,11 @@ __global__ void __launch_bounds__(kTileBlock) tile_kernel(DevNet net, DevState s
     unsigned long long it6 = 0, it4 = 0;
     int fails = 0;
     if ((sm_id() & 1u) == 0) {
-        tile_phase<6>(net, st, cfg, w.ovf6, &w.ctr[2], &w.ctr[4], smem, &it6, &fails);
-        tile_phase<4>(net, st, cfg, w.ovf4, &w.ctr[3], &w.ctr[5], smem, &it4, &fails);
+        tile_phase<6>(net, st, cfg, w.ovf6, &w.ctr[2], &w.ctr[4], smem, &it6, &fails, &sc->exec6);
+        tile_phase<4>(net, st, cfg, w.ovf4, &w.ctr[3], &w.ctr[5], smem, &it4, &fails, &sc->exec4);
     } else {
-        tile_phase<4>(net, st, cfg, w.ovf4, &w.ctr[3], &w.ctr[5], smem, &it4, &fails);
-        tile_phase<6>(net, st, cfg, w.ovf6, &w.ctr[2], &w.ctr[4], smem, &it6, &fails);
+        tile_phase<4>(net, st, cfg, w.ovf4, &w.ctr[3], &w.ctr[5], smem, &it4, &fails, &sc->exec4);
+        tile_phase<6>(net, st, cfg, w.ovf6, &w.ctr[2], &w.ctr[4], smem, &it6, &fails, &sc->exec6);
     }
     if ((threadIdx.x & (kTile - 1)) == 0) {
         if (it6) atomicAdd(&sc->tron_iters6, it6);

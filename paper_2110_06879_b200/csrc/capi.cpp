@@ -477,6 +477,14 @@ gridadmm_status gridadmm_session_counters(const gridadmm_session* s, long long* 
     });
 }
 
+gridadmm_status gridadmm_session_step_counters(const gridadmm_session* s, long long* out) {
+    if (!s || !out) return fail(GRIDADMM_ERR_INVALID_ARG, "null argument to step_counters");
+    return guarded([&]() -> gridadmm_status {
+        s->s->step_counters(out);
+        return GRIDADMM_OK;
+    });
+}
+
 gridadmm_status gridadmm_session_branch_costs(const gridadmm_session* s, int* costs) {
     if (!s || !costs) return fail(GRIDADMM_ERR_INVALID_ARG, "null argument to branch_costs");
     return guarded([&]() -> gridadmm_status {

@@ -77,6 +77,8 @@ struct DevScalars {
     unsigned long long tron_iters6; // TRON iterations, rate-limited (6-var) branches
     int singular_bus;               // min singular bus index, INT_MAX if none
     int pad;
+    unsigned long long exec4;       // trust-region steps actually executed (4-var)
+    unsigned long long exec6;       // (6-var); < TRON iterations when fixed points are skipped
 };
 
 struct BranchCfg {
@@ -86,7 +88,7 @@ struct BranchCfg {
     int max_cg = 32;
     double delta_floor = 1e-3;
     double limit_tighten = 0.99;
-    int lane_budget = 8;  // TRON iterations a branch may take in the lane phase
+    int lane_budget = 4;  // TRON iterations a branch may take in the lane phase (swept: 4 best)
 };
 
 // ---- launchers (kernels.cu / branch.cu) ----------------------------------

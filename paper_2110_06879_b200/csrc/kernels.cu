@@ -258,6 +258,245 @@ __global__ void __launch_bounds__(kBlock) bus_kernel(DevNet n, DevState s, DevSc
     block_max_atomic<1>(vals, dst);
 }
 
+// Warp-per-bus variant (the one launched).  The thread-per-bus kernel above
+// walks each bus's CSR rows four times as chains of dependent gathers and is
+// latency-bound with a long tail on high-degree buses; here the 32 lanes of
+// a warp gather the bus's rows in parallel into shared memory once (rho,
+// c = rho(x+z)+y, old xbar), lane 0 runs the ordered sums and the 3x3
+// elimination exactly as above, and the lanes write the rows back in
+// parallel.  Same arithmetic, same order, same bits.
+constexpr int kBusWarps = 8;
+constexpr int kBusCap = 96;  // staged rows per bus; larger buses read the rest from global
+
+// Gaussian elimination with partial pivoting on the NC x NC system
+// (kernels.cpp:364-391) with register-resident rows: the reference permutes
+// row indices (piv), here the rows themselves are swapped — the same values
+// meet the same operations, so the result is identical.  S is row-major 3x3.
+template <int NC>
+__device__ __forceinline__ bool ge_solve(double* S, double* rhs, double* mu) {
+    double A[NC][NC], b[NC];
+#pragma unroll
+    for (int r = 0; r < NC; ++r) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) A[r][c] = S[r * 3 + c];
+        b[r] = rhs[r];
+    }
+#pragma unroll
+    for (int col = 0; col < NC; ++col) {
+        int best = col;
+#pragma unroll
+        for (int r = col + 1; r < NC; ++r)
+            if (fabs(A[r][col]) > fabs(A[best][col])) best = r;
+#pragma unroll
+        for (int r = col + 1; r < NC; ++r) {
+            if (best == r) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const double t = A[col][c];
+                    A[col][c] = A[r][c];
+                    A[r][c] = t;
+                }
+                const double t = b[col];
+                b[col] = b[r];
+                b[r] = t;
+            }
+        }
+        const double d = A[col][col];
+        if (fabs(d) < 1e-14) return false;
+#pragma unroll
+        for (int r = col + 1; r < NC; ++r) {
+            const double f = A[r][col] / d;
+#pragma unroll
+            for (int s2 = col; s2 < NC; ++s2) A[r][s2] -= f * A[col][s2];
+            b[r] -= f * b[col];
+        }
+    }
+#pragma unroll
+    for (int col = NC - 1; col >= 0; --col) {
+        double acc = b[col];
+#pragma unroll
+        for (int s2 = col + 1; s2 < NC; ++s2) acc -= A[col][s2] * mu[s2];
+        mu[col] = acc / A[col][col];
+    }
+    return true;
+}
+
+__global__ void __launch_bounds__(kBusWarps * 32) bus_warp_kernel(DevNet n, DevState s,
+                                                                  DevScalars* sc) {
+    __shared__ double sq[kBusWarps][kBusCap], scv[kBusWarps][kBusCap], sxb[kBusWarps][kBusCap];
+    __shared__ double sts[kBusWarps][kBusCap], str[kBusWarps][kBusCap];  // S / rhs terms of dup rows
+    __shared__ double sres[kBusWarps][6];  // mu0..2, w, theta, singular flag
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    double dual = 0.0;
+    for (int i = blockIdx.x * kBusWarps + wib; i < n.nb; i += gridDim.x * kBusWarps) {
+        const int* grp = n.bus_grp + 7 * i;
+        int g[7];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) g[k] = grp[k];
+        const int cnt = g[6] - g[0];
+        const int* rows = n.bus_rows + g[0];
+        for (int k = lane; k < cnt && k < kBusCap; k += 32) {
+            const int row = rows[k];
+            const double q = s.rho[row];
+            const double c = q * (s.x[row] + s.z[row]) + s.y[row];
+            sq[wib][k] = q;
+            scv[wib][k] = c;
+            sxb[wib][k] = s.xbar[row];
+            // the per-column terms of the S / rhs sums (kernels.cpp:350-361)
+            // are independent of each other: form them in parallel here and
+            // leave only the ordered additions to lane 0
+            if (k >= g[2] - g[0]) {
+                const bool plus = k < g[4] - g[0];  // gen_p / gen_q columns carry +1, flows -1
+                const double a = plus ? 1.0 : -1.0;
+                sts[wib][k] = a * a / q;
+                str[wib][k] = a * c / q;
+            }
+        }
+        __syncwarp();
+        const bool ref = i == n.ref_bus;
+        const int nc = ref ? 3 : 2;
+        const double gs = n.b_gs[i], bs = n.b_bs[i];
+        auto cq = [&](int k, double* c, double* q) {  // local row k -> (c, rho)
+            if (k < kBusCap) { *c = scv[wib][k]; *q = sq[wib][k]; return; }
+            const int row = rows[k];
+            *q = s.rho[row];
+            *c = *q * (s.x[row] + s.z[row]) + s.y[row];
+        };
+        if (lane == 0) {
+            double q0 = 0.0, c0 = 0.0, q1 = 0.0, c1 = 0.0, c, q;
+            for (int k = 0; k < g[1] - g[0]; ++k) { cq(k, &c, &q); q0 += q; c0 += c; }
+            for (int k = g[1] - g[0]; k < g[2] - g[0]; ++k) { cq(k, &c, &q); q1 += q; c1 += c; }
+            if (q0 == 0.0) q0 = 1.0;
+            if (q1 == 0.0) q1 = 1.0;
+            bool finite = sfinite(c0) && sfinite(c1);
+            for (int k = g[2] - g[0]; k < cnt && finite; ++k) { cq(k, &c, &q); finite = sfinite(c); }
+            double S[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, rhs[3] = {0, 0, 0};
+            const double bvec[3] = {n.b_pd[i], n.b_qd[i], 0.0};
+            if (finite) {
+                const double a00 = -gs, a10 = bs;
+                double s00 = 0.0, s01 = 0.0, s11 = 0.0, s22 = 0.0, r0 = 0.0, r1 = 0.0, r2 = 0.0;
+                s00 += a00 * a00 / q0;
+                s01 += a00 * a10 / q0;
+                s11 += a10 * a10 / q0;
+                r0 += a00 * c0 / q0;
+                r1 += a10 * c0 / q0;
+                if (ref) {
+                    s22 += 1.0 * 1.0 / q1;
+                    r2 += 1.0 * c1 / q1;
+                }
+                // staged terms (same expressions as below, formed in parallel)
+                auto term = [&](int k, double a, double* ts, double* tr) {
+                    if (k < kBusCap) { *ts = sts[wib][k]; *tr = str[wib][k]; return; }
+                    cq(k, &c, &q);
+                    *ts = a * a / q;
+                    *tr = a * c / q;
+                };
+                double ts, tr;
+                for (int k = g[2] - g[0]; k < g[3] - g[0]; ++k) {  // gen_p (+1)
+                    term(k, 1.0, &ts, &tr);
+                    s00 += ts;
+                    r0 += tr;
+                }
+                for (int k = g[4] - g[0]; k < g[5] - g[0]; ++k) {  // flow_p (-1)
+                    term(k, -1.0, &ts, &tr);
+                    s00 += ts;
+                    r0 += tr;
+                }
+                for (int k = g[3] - g[0]; k < g[4] - g[0]; ++k) {  // gen_q (+1)
+                    term(k, 1.0, &ts, &tr);
+                    s11 += ts;
+                    r1 += tr;
+                }
+                for (int k = g[5] - g[0]; k < g[6] - g[0]; ++k) {  // flow_q (-1)
+                    term(k, -1.0, &ts, &tr);
+                    s11 += ts;
+                    r1 += tr;
+                }
+                S[0] = s00; S[1] = s01; S[3] = s01; S[4] = s11;
+                S[8] = s22;
+                rhs[0] = r0 - bvec[0];
+                rhs[1] = r1 - bvec[1];
+                rhs[2] = r2 - bvec[2];
+            } else {
+                // dense reference loop (kernels.cpp:350-361)
+                auto col = [&](int j, int* gg, double* qj, double* cj) {
+                    if (j == 0) { *gg = 0; *qj = q0; *cj = c0; return; }
+                    if (j == 1) { *gg = 1; *qj = q1; *cj = c1; return; }
+                    const int k = g[2] - g[0] + (j - 2);
+                    int grp_id = 2;
+                    while (k >= g[grp_id + 1] - g[0]) ++grp_id;
+                    *gg = grp_id;
+                    cq(k, cj, qj);
+                };
+                const int nv = 2 + (g[6] - g[2]);
+                for (int r = 0; r < nc; ++r) {
+                    for (int t = 0; t < nc; ++t) {
+                        double acc = 0.0;
+                        for (int j = 0; j < nv; ++j) {
+                            int gg; double qj, cj;
+                            col(j, &gg, &qj, &cj);
+                            acc += a_coef(r, gg, gs, bs, ref) * a_coef(t, gg, gs, bs, ref) / qj;
+                        }
+                        S[r * 3 + t] = acc;
+                    }
+                    double acc = 0.0;
+                    for (int j = 0; j < nv; ++j) {
+                        int gg; double qj, cj;
+                        col(j, &gg, &qj, &cj);
+                        acc += a_coef(r, gg, gs, bs, ref) * cj / qj;
+                    }
+                    rhs[r] = acc - bvec[r];
+                }
+            }
+            double mu[3] = {0, 0, 0};
+            const bool singular = ref ? !ge_solve<3>(S, rhs, mu) : !ge_solve<2>(S, rhs, mu);
+            if (!singular) {
+                double acc = c0;
+                for (int r = 0; r < nc; ++r) acc -= a_coef(r, 0, gs, bs, ref) * mu[r];
+                sres[wib][3] = acc / q0;
+                acc = c1;
+                for (int r = 0; r < nc; ++r) acc -= a_coef(r, 1, gs, bs, ref) * mu[r];
+                sres[wib][4] = acc / q1;
+                s.bus_w[i] = sres[wib][3];
+                s.bus_theta[i] = sres[wib][4];
+            } else {
+                atomicMin(&sc->singular_bus, i);
+            }
+            sres[wib][0] = mu[0];
+            sres[wib][1] = mu[1];
+            sres[wib][2] = mu[2];
+            sres[wib][5] = singular ? 1.0 : 0.0;
+        }
+        __syncwarp();
+        if (sres[wib][5] == 0.0) {
+            const double mu[3] = {sres[wib][0], sres[wib][1], sres[wib][2]};
+            const double w = sres[wib][3], th = sres[wib][4];
+            for (int k = lane; k < cnt; k += 32) {
+                const int row = rows[k];
+                double v;
+                if (k < g[1] - g[0]) v = w;
+                else if (k < g[2] - g[0]) v = th;
+                else {
+                    int gg = 2;
+                    while (k >= g[gg + 1] - g[0]) ++gg;
+                    double c, q;
+                    cq(k, &c, &q);
+                    double acc = c;
+                    for (int r = 0; r < nc; ++r) acc -= a_coef(r, gg, gs, bs, ref) * mu[r];
+                    v = acc / q;
+                }
+                const double old = k < kBusCap ? sxb[wib][k] : s.xbar[row];
+                dual = smax(dual, abs_or_zero(v - old));
+                s.xbar[row] = v;
+            }
+        }
+        __syncwarp();
+    }
+    double vals[1] = {dual};
+    unsigned long long* const dst[1] = {&sc->dual_inf};
+    block_max_atomic<1>(vals, dst);
+}
+
 // ---- fused z / y / residual (kernels.cpp:415-428, decomp.cpp:59-72) -----
 __global__ void __launch_bounds__(kBlock) zy_kernel(DevNet n, DevState s, double beta,
                                                     DevScalars* sc) {
@@ -387,6 +626,22 @@ void launch_generators(const DevNet& n, const DevState& s, cudaStream_t st) {
 }
 
 void launch_buses(const DevNet& n, const DevState& s, DevScalars* sc, cudaStream_t st) {
+    if (n.nb <= 0) return;
+    static int max_blocks = 0;
+    if (max_blocks == 0) {
+        int dev = 0, sms = 148, per_sm = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bus_warp_kernel, kBusWarps * 32, 0);
+        max_blocks = sms * (per_sm > 0 ? per_sm : 1);
+    }
+    int blocks = (n.nb + kBusWarps - 1) / kBusWarps;
+    if (blocks > max_blocks) blocks = max_blocks;
+    bus_warp_kernel<<<blocks, kBusWarps * 32, 0, st>>>(n, s, sc);
+}
+
+// Reference-shaped one-thread-per-bus kernel (kept for A/B timing).
+void launch_buses_thread(const DevNet& n, const DevState& s, DevScalars* sc, cudaStream_t st) {
     if (n.nb > 0) bus_kernel<<<blocks_for(n.nb), kBlock, 0, st>>>(n, s, sc);
 }
 

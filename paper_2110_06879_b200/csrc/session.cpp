@@ -288,6 +288,13 @@ void Session::clamp_gen_p() {
 BranchCfg branch_cfg(const SolverConfig& c) {
     BranchCfg b = c.tron;
     b.limit_tighten = c.limit_tighten;
+    // Scheduling knob only (results are schedule-independent): TRON steps a
+    // branch may take in the lane phase before moving to the tile phase.
+    static const int budget = [] {
+        const char* e = std::getenv("GRIDADMM_LANE_BUDGET");
+        return e ? std::atoi(e) : -1;
+    }();
+    if (budget >= 1) b.lane_budget = budget;
     return b;
 }
 
@@ -408,6 +415,15 @@ long long Session::sincos_calls() const {
     DevScalars h;
     check(cudaMemcpy(&h, sc_, sizeof h, cudaMemcpyDeviceToHost), "D2H");
     return static_cast<long long>(h.tron_iters6);
+}
+
+void Session::step_counters(long long out[4]) const {
+    DevScalars h;
+    check(cudaMemcpy(&h, sc_, sizeof h, cudaMemcpyDeviceToHost), "D2H");
+    out[0] = static_cast<long long>(h.tron_iters4);
+    out[1] = static_cast<long long>(h.tron_iters6);
+    out[2] = static_cast<long long>(h.exec4);
+    out[3] = static_cast<long long>(h.exec6);
 }
 
 void Session::branch_costs(int* out) const {

@@ -140,6 +140,8 @@ public:
     KernelClock kernel_clock(int cls) const { return clocks_[cls]; }
     long long tron_iterations() const;
     void branch_costs(int* out) const;
+    // TRON iterations (reference semantics) and executed steps, 4-/6-var.
+    void step_counters(long long out[4]) const;
     long long sincos_calls() const;
     void sync() const;
 

@@ -50,6 +50,16 @@ constexpr double kTronDeltaMax = 1e10; // tron.cpp:12
 
 enum TronStatusCode : int { kTronConverged = 0, kTronIterationLimit = 1, kTronNumericalError = 2 };
 
+GA_FN long long __double_as_longlong_portable(double v) {
+#if defined(__CUDA_ARCH__)
+    return __double_as_longlong(v);
+#else
+    long long r;
+    __builtin_memcpy(&r, &v, sizeof r);
+    return r;
+#endif
+}
+
 // ---- sequential reductions over N (tron.cpp:16-51) ------------------------
 
 template <int N>
@@ -503,14 +513,29 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
     const double pred = -q;
     const double ratio = pred > 0.0 ? ared / pred : (ared > 0.0 ? 1.0 : -1.0);
     const double snorm = vnorm2<N>(stp);
+    const double delta_used = st.delta;
     if (ratio < 0.25) st.delta = 0.25 * smax(snorm, 1e-12);
     else if (ratio > 0.75 && snorm >= 0.9 * st.delta) st.delta = smin(2.0 * st.delta, kTronDeltaMax);
-    if (ared > 0.0 && ratio > kTronEta) {
+    const bool accepted = ared > 0.0 && ratio > kTronEta;
+    if (accepted) {
 #pragma unroll
         for (int i = 0; i < N; ++i) st.x[i] = xt[i];
         st.f = ft;
+    } else {
+        GA_STAT(6);  // rejected step: x (hence g, H) unchanged
     }
+    if (st.iter >= 100) GA_STAT(7);  // steps of solves deep in the tail
     ++st.iter;
+    // Fixed point: a rejected step that leaves the radius bit-identical
+    // leaves the whole iterate (x, f, delta) unchanged, and an iteration with
+    // iter >= 1 is a pure function of (x, f, delta) — so every remaining
+    // iteration up to the cap would recompute exactly this one.  The
+    // reference executes them (tron.cpp:243-317); jumping to the cap gives
+    // the identical final state and TronResult (iterations = max_iterations).
+    if (!accepted && __double_as_longlong_portable(st.delta) == __double_as_longlong_portable(delta_used)) {
+        GA_STAT(5);
+        st.iter = cfg.max_iterations;
+    }
     if (st.delta < 1e-14 || st.iter >= cfg.max_iterations) return kStepExhausted;
     return kStepContinue;
 }

@@ -19,7 +19,7 @@ ga.lib().gridadmm_debug_tron_stats(buf, 1)
 ms, _ = s.timed_steps(1, 0)
 ga.lib().gridadmm_debug_tron_stats(buf, 1)
 st = list(buf)
-names = ["steps", "cauchy_extrap", "cauchy_halve", "cg_iters", "ls_steps", "chol_fail"]
+names = ["steps", "cauchy_extrap", "cauchy_halve", "cg_iters", "ls_steps", "chol_fail", "rejected", "iter>=100"]
 print("iteration", n_it - 1, "ms", ms[0])
 for k, nm in enumerate(names):
     print(f"{nm:14s} {st[k]:12d}  per step {st[k] / max(1, st[0]):.3f}")

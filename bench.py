@@ -62,7 +62,7 @@ def parse():
     ap.add_argument("--shape", default=SHAPE)
     ap.add_argument("--seed", type=int, default=2110)
     ap.add_argument("--preset", default="case_ACTIVSg70k")
-    ap.add_argument("--cpu-steps", type=int, default=6, help="timed iterations of the CPU sample")
+    ap.add_argument("--cpu-steps", type=int, default=30, help="timed iterations of the CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -227,13 +227,13 @@ def run_b200(args, d: Dist):
     sess = ga.Session(net, cfg)
     sess.timed_steps(args.warmup, 0)  # warm-up iterations (untimed)
     k0 = [sess.kernel_time(c) for c in range(4)]
-    it0 = sess.counters()
+    it0 = sess.step_counters()
     d.barrier()
     with ClockSampler(dev) as clk:
         step_ms, rec = sess.timed_steps(args.steps, L2_FLUSH_BYTES)
     d.barrier()
     k1 = [sess.kernel_time(c) for c in range(4)]
-    it1 = sess.counters()
+    it1 = sess.step_counters()
     my_ms = float(np.sum(step_ms))
     max_ms = d.max(my_ms)
     total_iters = d.sum(float(args.steps))
@@ -241,14 +241,22 @@ def run_b200(args, d: Dist):
 
     kern = {name: {"ms_total": k1[c][0] - k0[c][0], "launches": k1[c][1] - k0[c][1]}
             for c, name in enumerate(["generators", "branches", "buses", "zy"])}
-    tron4 = it1[0] - it0[0]
-    tron6 = it1[1] - it0[1]
+    # reference-accounted TRON iterations vs trust-region steps the device
+    # executed (exact fixed points are skipped, tron.cuh); the roofline counts
+    # executed work only
+    tron4, tron6 = it1[0] - it0[0], it1[1] - it0[1]
+    exec4, exec6 = it1[2] - it0[2], it1[3] - it0[3]
     branch_ms = kern["branches"]["ms_total"]
-    flops = tron4 * CENSUS_FLOPS[4] + tron6 * CENSUS_FLOPS[6]
+    flops = exec4 * CENSUS_FLOPS[4] + exec6 * CENSUS_FLOPS[6]
+    ref_flops = tron4 * CENSUS_FLOPS[4] + tron6 * CENSUS_FLOPS[6]
     fp64_mul_add, fp64_fma = ga.fp64_peak(dev)
     achieved = flops / (branch_ms * 1e-3) / 1e12 if branch_ms > 0 else 0.0
     # HBM-bound phases: algorithmic bytes per iteration
-    hbm_bytes = {"generators": 128 * ng, "buses": 44 * m + 72 * nb, "zy": 64 * m}
+    # generators: 4 row arrays x 2 rows + 6 params read, 2 rows written;
+    # buses: per row index + rho, x, z, y, xbar read and xbar written, per bus
+    # 7 CSR offsets + gs, bs, pd, qd read and w, theta written; zy: x, xbar,
+    # rho, z, y, lambda read, z, y written
+    hbm_bytes = {"generators": 128 * ng, "buses": 52 * m + 76 * nb, "zy": 64 * m}
     hbm = {}
     for name, b in hbm_bytes.items():
         t = kern[name]["ms_total"] / max(1, kern[name]["launches"])
@@ -263,11 +271,12 @@ def run_b200(args, d: Dist):
     # --- e2e through the C ABI (host buffers) -----------------------------
     e2e = None
     if not args.no_e2e:
-        cfg2 = ga.Config(args.preset, device=dev, max_outer=1, max_inner=args.warmup + args.steps)
+        n_e2e = max(args.warmup + args.steps, 200)
+        cfg2 = ga.Config(args.preset, device=dev, max_outer=1, max_inner=n_e2e)
+        net2 = ga.Network(path)  # host parse (file I/O) outside, like the reference's elapsed_s
         d.barrier()
         t0 = time.perf_counter()
-        net2 = ga.Network(path)  # host parse -> H2D inside the solve
-        st, rep = ga.solve(net2, cfg2)
+        st, rep = ga.solve(net2, cfg2)  # network + state H2D, iterations, solution D2H
         pg, qg = rep.dispatch()
         vm, va = rep.voltages()
         t_e2e = time.perf_counter() - t0
@@ -279,8 +288,9 @@ def run_b200(args, d: Dist):
         e2e = {"value": d.sum(n_it) / t_max, "unit": "iters/s",
                "h2d_bytes_per_step": h2d / n_it, "d2h_bytes_per_step": d2h / n_it,
                "wall_s": t_max, "iterations": int(n_it),
-               "note": "gridadmm_network_load + gridadmm_solve(max_outer=1) + dispatch/voltages; "
-                       "includes parse, upload, cold start, solution download"}
+               "note": "gridadmm_solve(max_outer=1) on a loaded network + dispatch/voltages: "
+                       "device alloc, network+state upload, cold start, every iteration's "
+                       "norm readback, solution download (file parse excluded)"}
 
     # --- CPU baseline (reference on host cores), rank 0 only ---------------
     cpu = None
@@ -321,7 +331,10 @@ def run_b200(args, d: Dist):
                          "peak_note": "measured DMUL+DADD issue rate (kernel built -fmad=false); "
                                       f"DFMA peak {fp64_fma:.1f} TFLOP/s",
                          "flops_per_launch": flops / max(1, kern["branches"]["launches"]),
-                         "tron_iterations": [tron4, tron6]},
+                         "tron_iterations_reference": [tron4, tron6],
+                         "tron_steps_executed": [exec4, exec6],
+                         "reference_equivalent_tflops": (ref_flops / (branch_ms * 1e-3) / 1e12
+                                                         if branch_ms > 0 else None)},
             "roofline_hbm": {k: dict(v, peak_gbs=hbm_peak,
                                      frac=(v["gbs"] / hbm_peak if v["gbs"] else None))
                              for k, v in hbm.items()},

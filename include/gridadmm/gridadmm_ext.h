@@ -64,6 +64,13 @@ gridadmm_status gridadmm_network_export(const gridadmm_network* net, double* bus
                                         int* bus_id, double* gen, int* ends,
                                         double* branch, int* ref_bus);
 
+/* Deterministic k-way bus-graph partition used when the config key
+ * `partitions` is k > 1 (host only): part_of_bus[i] in [0, k).  Branch b is
+ * solved by the part of its from-bus; per iteration a cut branch's four
+ * to-side rows (pji, qji, wj, thj) are exchanged (x forward, xbar/z/y back). */
+gridadmm_status gridadmm_network_partition(const gridadmm_network* net, int k,
+                                           int* part_of_bus);
+
 /* Bus-owned row lists of the coupling layout (proj/src/decomp.cpp:7-31):
  * counts[6*i + k] = sizes of (gen_p, gen_q, flow_p, flow_q, w, theta) of bus
  * i, rows = the lists concatenated per bus in that group order (length m). */

@@ -78,6 +78,7 @@ EXT_SYMBOLS = {
     "gridadmm_network_num_rows": (_I, [_P]),
     "gridadmm_network_export": (_I, [_P, _DP, _IP, _DP, _IP, _DP, _IP]),
     "gridadmm_network_layout": (_I, [_P, _IP, _IP]),
+    "gridadmm_network_partition": (_I, [_P, _I, _IP]),
     "gridadmm_session_new": (_I, [_P, _P, ctypes.POINTER(_P)]),
     "gridadmm_session_free": (None, [_P]),
     "gridadmm_session_get_state": (_I, [_P, ctypes.POINTER(StateView)]),
@@ -189,6 +190,12 @@ class Network:
                                              ends.ctypes.data_as(_IP), _dp(br), ctypes.byref(ref)))
         return {"bus": bus.reshape(-1, 6), "bus_id": ids, "gen": gen.reshape(-1, 8),
                 "ends": ends.reshape(-1, 2), "branch": br.reshape(-1, 14), "ref_bus": ref.value}
+
+    def partition(self, k: int) -> np.ndarray:
+        """part_of_bus of the deterministic k-way partition (gridadmm_network_partition)."""
+        out = np.zeros(max(1, self.num_buses), dtype=np.int32)
+        _check(lib().gridadmm_network_partition(self._h, k, out.ctypes.data_as(_IP)))
+        return out[: self.num_buses]
 
     def layout(self):
         counts = np.zeros(6 * self.num_buses, dtype=np.int32)

@@ -63,7 +63,8 @@ struct gridadmm_track {
     ga::Network net;
 };
 struct gridadmm_session {
-    std::unique_ptr<ga::Session> s;
+    std::unique_ptr<ga::Engine> e;  // one Session or a MultiPart (config `partitions` > 1)
+    ga::Session* s = nullptr;       // == e when single-part (kernel-level helpers)
 };
 
 namespace {
@@ -102,6 +103,11 @@ const std::map<std::string, Field>& fields() {
                        [](gridadmm_config& c, double v) { c.ramp_frac = v; }}},
         {"device", {true, 0.0, [](const gridadmm_config& c) { return double(c.solver.device); },
                     [](gridadmm_config& c, double v) { c.solver.device = int(v); }}},
+        // bus-graph partition (multi.cpp): parts, and GPUs they are spread over
+        {"partitions", {true, 1.0, [](const gridadmm_config& c) { return double(c.solver.partitions); },
+                        [](gridadmm_config& c, double v) { c.solver.partitions = int(v); }}},
+        {"devices", {true, 1.0, [](const gridadmm_config& c) { return double(c.solver.devices); },
+                     [](gridadmm_config& c, double v) { c.solver.devices = int(v); }}},
     };
     return f;
 }
@@ -182,6 +188,13 @@ gridadmm_status gridadmm_network_export(const gridadmm_network* n, double* bus, 
     return GRIDADMM_OK;
 }
 
+gridadmm_status gridadmm_network_partition(const gridadmm_network* n, int k, int* part_of_bus) {
+    if (!n || !part_of_bus || k < 1) return fail(GRIDADMM_ERR_INVALID_ARG, "bad argument to partition");
+    const std::vector<int> part = ga::partition_buses(n->net, k);
+    std::memcpy(part_of_bus, part.data(), part.size() * sizeof(int));
+    return GRIDADMM_OK;
+}
+
 gridadmm_status gridadmm_network_layout(const gridadmm_network* n, int* counts, int* rows) {
     if (!n) return fail(GRIDADMM_ERR_INVALID_ARG, "null network");
     const ga::BusCsr csr = ga::build_bus_csr(n->net);
@@ -240,8 +253,8 @@ gridadmm_status gridadmm_solve(const gridadmm_network* net, const gridadmm_confi
                                gridadmm_report** out) {
     if (!net || !cfg || !out) return fail(GRIDADMM_ERR_INVALID_ARG, "null argument to solve");
     try {
-        ga::Session session(net->net, cfg->solver);
-        auto* rep = new gridadmm_report{ga::solve(session, cfg->solver, false), net->net};
+        std::unique_ptr<ga::Engine> eng = ga::make_engine(net->net, cfg->solver);
+        auto* rep = new gridadmm_report{ga::solve(*eng, cfg->solver, false), net->net};
         *out = rep;
         const gridadmm_status s = status_of(rep->report.status);
         if (s != GRIDADMM_OK)
@@ -365,8 +378,9 @@ gridadmm_status gridadmm_session_new(const gridadmm_network* net, const gridadmm
     if (!net || !cfg || !out) return fail(GRIDADMM_ERR_INVALID_ARG, "null argument to session_new");
     return guarded([&]() -> gridadmm_status {
         auto h = std::make_unique<gridadmm_session>();
-        h->s = std::make_unique<ga::Session>(net->net, cfg->solver);
-        h->s->cold_start();
+        h->e = ga::make_engine(net->net, cfg->solver);
+        h->s = dynamic_cast<ga::Session*>(h->e.get());
+        h->e->cold_start();
         *out = h.release();
         return GRIDADMM_OK;
     });
@@ -378,7 +392,7 @@ gridadmm_status gridadmm_session_get_state(const gridadmm_session* s, const grid
     if (!s || !v) return fail(GRIDADMM_ERR_INVALID_ARG, "null argument to session_get_state");
     return guarded([&]() -> gridadmm_status {
         ga::HostState h;
-        s->s->download_state(h);
+        s->e->download_state(h);
         auto cp = [](const std::vector<double>& src, double* dst) {
             if (dst && !src.empty()) std::memcpy(dst, src.data(), src.size() * sizeof(double));
         };
@@ -394,7 +408,7 @@ gridadmm_status gridadmm_session_get_state(const gridadmm_session* s, const grid
 gridadmm_status gridadmm_session_set_state(gridadmm_session* s, const gridadmm_state_view* v) {
     if (!s || !v) return fail(GRIDADMM_ERR_INVALID_ARG, "null argument to session_set_state");
     return guarded([&]() -> gridadmm_status {
-        const ga::Network& n = s->s->network();
+        const ga::Network& n = s->e->network();
         const size_t m = n.m(), nb = n.nb(), nl = n.nl();
         ga::HostState h;
         auto cp = [](std::vector<double>& dst, const double* src, size_t count) {
@@ -404,8 +418,8 @@ gridadmm_status gridadmm_session_set_state(gridadmm_session* s, const gridadmm_s
         cp(h.lambda, v->lambda, m); cp(h.rho, v->rho, m); cp(h.bus_w, v->bus_w, nb);
         cp(h.bus_theta, v->bus_theta, nb); cp(h.bp, v->branch_point, 6 * nl);
         cp(h.lt_ij, v->lt_ij, nl); cp(h.lt_ji, v->lt_ji, nl); cp(h.rho_t, v->rho_tilde, nl);
-        h.beta = v->beta ? *v->beta : s->s->beta();
-        s->s->upload_state(h);
+        h.beta = v->beta ? *v->beta : s->e->beta();
+        s->e->upload_state(h);
         return GRIDADMM_OK;
     });
 }
@@ -413,6 +427,7 @@ gridadmm_status gridadmm_session_set_state(gridadmm_session* s, const gridadmm_s
 gridadmm_status gridadmm_session_phase(gridadmm_session* s, int phase, double* aux) {
     if (!s) return fail(GRIDADMM_ERR_INVALID_ARG, "null session");
     if (phase < 0 || phase > 5) return fail(GRIDADMM_ERR_INVALID_ARG, "unknown phase");
+    if (!s->s) return fail(GRIDADMM_ERR_INVALID_ARG, "phase replay needs a single-part session");
     return guarded([&]() -> gridadmm_status {
         const double zi = (phase == 5 && aux) ? aux[0] : 0.0;
         const double pz = (phase == 5 && aux) ? aux[1] : -1.0;
@@ -426,13 +441,13 @@ gridadmm_status gridadmm_session_iterate(gridadmm_session* s, int n, double* rec
                                          int* stop) {
     if (!s || n < 0) return fail(GRIDADMM_ERR_INVALID_ARG, "bad argument to session_iterate");
     return guarded([&]() -> gridadmm_status {
-        const ga::SolverConfig& cfg = s->s->config();
-        const double inner_tol = cfg.effective_inner_tol(s->s->m());
-        const double rho_max = s->s->rho_max();
+        const ga::SolverConfig& cfg = s->e->config();
+        const double inner_tol = cfg.effective_inner_tol(s->e->m());
+        const double rho_max = s->e->rho_max();
         int k = 0, why = 0;
         for (; k < n; ++k) {
             double nrm[4];
-            const int fails = s->s->iterate(nrm, nullptr);
+            const int fails = s->e->iterate(nrm, nullptr);
             const double primal = nrm[0], dual = nrm[1] * rho_max, z = nrm[2];
             if (records) {
                 double* r = records + 5 * k;
@@ -452,6 +467,7 @@ gridadmm_status gridadmm_session_iterate(gridadmm_session* s, int n, double* rec
 gridadmm_status gridadmm_session_timed_steps(gridadmm_session* s, int n, size_t flush_bytes,
                                              double* step_ms, double* records) {
     if (!s || n < 0) return fail(GRIDADMM_ERR_INVALID_ARG, "bad argument to session_timed_steps");
+    if (!s->s) return fail(GRIDADMM_ERR_INVALID_ARG, "timed_steps needs a single-part session");
     return guarded([&]() -> gridadmm_status {
         s->s->timed_steps(n, flush_bytes, step_ms, records);
         return GRIDADMM_OK;
@@ -461,6 +477,7 @@ gridadmm_status gridadmm_session_timed_steps(gridadmm_session* s, int n, size_t 
 gridadmm_status gridadmm_session_kernel_time(const gridadmm_session* s, int cls, double* ms,
                                              long long* launches) {
     if (!s || cls < 0 || cls > 3) return fail(GRIDADMM_ERR_INVALID_ARG, "bad argument to kernel_time");
+    if (!s->s) return fail(GRIDADMM_ERR_INVALID_ARG, "kernel_time needs a single-part session");
     const ga::KernelClock c = s->s->kernel_clock(cls);
     if (ms) *ms = c.ms;
     if (launches) *launches = c.launches;
@@ -469,7 +486,7 @@ gridadmm_status gridadmm_session_kernel_time(const gridadmm_session* s, int cls,
 
 gridadmm_status gridadmm_session_counters(const gridadmm_session* s, long long* tron_iterations,
                                           long long* sincos_calls) {
-    if (!s) return fail(GRIDADMM_ERR_INVALID_ARG, "null session");
+    if (!s || !s->s) return fail(GRIDADMM_ERR_INVALID_ARG, "counters need a single-part session");
     return guarded([&]() -> gridadmm_status {
         if (tron_iterations) *tron_iterations = s->s->tron_iterations();
         if (sincos_calls) *sincos_calls = s->s->sincos_calls();
@@ -478,7 +495,7 @@ gridadmm_status gridadmm_session_counters(const gridadmm_session* s, long long* 
 }
 
 gridadmm_status gridadmm_session_step_counters(const gridadmm_session* s, long long* out) {
-    if (!s || !out) return fail(GRIDADMM_ERR_INVALID_ARG, "null argument to step_counters");
+    if (!s || !out || !s->s) return fail(GRIDADMM_ERR_INVALID_ARG, "bad argument to step_counters");
     return guarded([&]() -> gridadmm_status {
         s->s->step_counters(out);
         return GRIDADMM_OK;
@@ -486,7 +503,7 @@ gridadmm_status gridadmm_session_step_counters(const gridadmm_session* s, long l
 }
 
 gridadmm_status gridadmm_session_branch_costs(const gridadmm_session* s, int* costs) {
-    if (!s || !costs) return fail(GRIDADMM_ERR_INVALID_ARG, "null argument to branch_costs");
+    if (!s || !costs || !s->s) return fail(GRIDADMM_ERR_INVALID_ARG, "bad argument to branch_costs");
     return guarded([&]() -> gridadmm_status {
         s->s->branch_costs(costs);
         return GRIDADMM_OK;

@@ -41,6 +41,19 @@ struct DevNet {
     double *b_vmin = nullptr, *b_vmax = nullptr;
     int* bus_grp = nullptr;   // [7*nb] group offsets into bus_rows
     int* bus_rows = nullptr;  // [m]
+    // ownership subset of a multi-part run (partition.hpp); nullptr = all.
+    // lim_list / unl_list above already hold only the owned branches.
+    int* own_gens = nullptr;
+    int* own_buses = nullptr;
+    int* own_rows = nullptr;
+    int n_own_gens = 0, n_own_buses = 0, n_own_rows = 0;
+
+    __host__ __device__ int gens_count() const { return own_gens ? n_own_gens : ng; }
+    __host__ __device__ int buses_count() const { return own_buses ? n_own_buses : nb; }
+    __host__ __device__ int rows_count() const { return own_rows ? n_own_rows : m; }
+    __host__ __device__ int gen_at(int t) const { return own_gens ? own_gens[t] : t; }
+    __host__ __device__ int bus_at(int t) const { return own_buses ? own_buses[t] : t; }
+    __host__ __device__ int row_at(int t) const { return own_rows ? own_rows[t] : t; }
 };
 
 struct DevState {
@@ -107,6 +120,10 @@ void launch_outer(const DevNet& n, const DevState& s, double beta, double lam_mi
 void launch_reset_scalars(DevScalars* sc, cudaStream_t st);
 // max(0, max_k v[k]) with NaN skipped (driver.cpp:179-183 rho_max), as bits.
 void launch_rowmax(const double* v, int n, unsigned long long* dst, cudaStream_t st);
+// Boundary exchange of multi-part runs (partition.hpp).
+void launch_copy_rows(const int* rows, int count, const double* src, double* dst, cudaStream_t st);
+void launch_gather_rows(const int* rows, int count, const double* v, double* buf, cudaStream_t st);
+void launch_scatter_rows(const int* rows, int count, const double* buf, double* v, cudaStream_t st);
 // Tracking carry-over: clamp x/xbar p-rows into [pmin, pmax] (tracking.cpp:65-70).
 void launch_clamp_gen_p(const DevNet& n, const DevState& s, cudaStream_t st);
 // Batched TRON on dense box QPs (parity test of the TRON core).

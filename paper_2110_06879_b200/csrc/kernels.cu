@@ -53,8 +53,9 @@ __device__ __forceinline__ void block_max_atomic(double (&v)[NV], unsigned long 
 
 // ---- generators (kernels.cpp:194-209) ----------------------------------
 __global__ void __launch_bounds__(kBlock) gen_kernel(DevNet n, DevState s) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= n.ng) return;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n.gens_count()) return;
+    const int g = n.gen_at(t);
     // rows 2g, 2g+1 are adjacent: one 16-B load per array
     const double2 xb = reinterpret_cast<const double2*>(s.xbar)[g];
     const double2 zz = reinterpret_cast<const double2*>(s.z)[g];
@@ -328,7 +329,9 @@ __global__ void __launch_bounds__(kBusWarps * 32) bus_warp_kernel(DevNet n, DevS
     __shared__ double sres[kBusWarps][6];  // mu0..2, w, theta, singular flag
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     double dual = 0.0;
-    for (int i = blockIdx.x * kBusWarps + wib; i < n.nb; i += gridDim.x * kBusWarps) {
+    const int nbus = n.buses_count();
+    for (int t = blockIdx.x * kBusWarps + wib; t < nbus; t += gridDim.x * kBusWarps) {
+        const int i = n.bus_at(t);
         const int* grp = n.bus_grp + 7 * i;
         int g[7];
 #pragma unroll
@@ -501,7 +504,9 @@ __global__ void __launch_bounds__(kBusWarps * 32) bus_warp_kernel(DevNet n, DevS
 __global__ void __launch_bounds__(kBlock) zy_kernel(DevNet n, DevState s, double beta,
                                                     DevScalars* sc) {
     double pr = 0.0, zi = 0.0, zd = 0.0;
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n.m; k += gridDim.x * blockDim.x) {
+    const int nrows = n.rows_count();
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nrows; t += gridDim.x * blockDim.x) {
+        const int k = n.row_at(t);
         const double x = s.x[k], xb = s.xbar[k], rho = s.rho[k];
         const double zold = s.z[k], y = s.y[k];
         const double r = x - xb;
@@ -519,27 +524,31 @@ __global__ void __launch_bounds__(kBlock) zy_kernel(DevNet n, DevState s, double
 }
 
 __global__ void z_only_kernel(DevNet n, DevState s, double beta) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n.m) return;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n.rows_count()) return;
+    const int k = n.row_at(t);
     const double r = s.x[k] - s.xbar[k];
     s.z[k] = -(s.lambda[k] + s.y[k] + s.rho[k] * r) / (s.rho[k] + beta);
 }
 
 __global__ void y_only_kernel(DevNet n, DevState s) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n.m) return;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n.rows_count()) return;
+    const int k = n.row_at(t);
     s.y[k] += s.rho[k] * (s.x[k] - s.xbar[k] + s.z[k]);
 }
 
 __global__ void outer_kernel(DevNet n, DevState s, double beta, double lmin, double lmax) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n.m) return;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n.rows_count()) return;
+    const int k = n.row_at(t);
     s.lambda[k] = sclamp(s.lambda[k] + beta * s.z[k], lmin, lmax);
 }
 
 __global__ void clamp_gen_p_kernel(DevNet n, DevState s) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= n.ng) return;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n.gens_count()) return;
+    const int g = n.gen_at(t);
     const int pr = 2 * g;
     s.x[pr] = sclamp(s.x[pr], n.g_pmin[g], n.g_pmax[g]);
     s.xbar[pr] = sclamp(s.xbar[pr], n.g_pmin[g], n.g_pmax[g]);
@@ -621,56 +630,102 @@ void measure_fp64_peak(double* tflops_mul_add, double* tflops_fma) {
     cudaFree(out);
 }
 
+namespace {
+int sm_count() {
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+}  // namespace
+
 void launch_generators(const DevNet& n, const DevState& s, cudaStream_t st) {
-    if (n.ng > 0) gen_kernel<<<blocks_for(n.ng), kBlock, 0, st>>>(n, s);
+    const int c = n.gens_count();
+    if (c > 0) gen_kernel<<<blocks_for(c), kBlock, 0, st>>>(n, s);
 }
 
 void launch_buses(const DevNet& n, const DevState& s, DevScalars* sc, cudaStream_t st) {
-    if (n.nb <= 0) return;
+    const int c = n.buses_count();
+    if (c <= 0) return;
     static int max_blocks = 0;
     if (max_blocks == 0) {
-        int dev = 0, sms = 148, per_sm = 1;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bus_warp_kernel, kBusWarps * 32, 0);
-        max_blocks = sms * (per_sm > 0 ? per_sm : 1);
+        max_blocks = sm_count() * (per_sm > 0 ? per_sm : 1);
     }
-    int blocks = (n.nb + kBusWarps - 1) / kBusWarps;
+    int blocks = (c + kBusWarps - 1) / kBusWarps;
     if (blocks > max_blocks) blocks = max_blocks;
     bus_warp_kernel<<<blocks, kBusWarps * 32, 0, st>>>(n, s, sc);
 }
 
-// Reference-shaped one-thread-per-bus kernel (kept for A/B timing).
+// Reference-shaped one-thread-per-bus kernel (kept for A/B timing; whole net).
 void launch_buses_thread(const DevNet& n, const DevState& s, DevScalars* sc, cudaStream_t st) {
     if (n.nb > 0) bus_kernel<<<blocks_for(n.nb), kBlock, 0, st>>>(n, s, sc);
 }
 
 void launch_zy(const DevNet& n, const DevState& s, double beta, DevScalars* sc,
                cudaStream_t st) {
-    if (n.m <= 0) return;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int blocks = blocks_for(n.m);
-    if (blocks > sms * 8) blocks = sms * 8;
+    const int c = n.rows_count();
+    if (c <= 0) return;
+    int blocks = blocks_for(c);
+    if (blocks > sm_count() * 8) blocks = sm_count() * 8;
     zy_kernel<<<blocks, kBlock, 0, st>>>(n, s, beta, sc);
 }
 
 void launch_z_only(const DevNet& n, const DevState& s, double beta, cudaStream_t st) {
-    if (n.m > 0) z_only_kernel<<<blocks_for(n.m), kBlock, 0, st>>>(n, s, beta);
+    const int c = n.rows_count();
+    if (c > 0) z_only_kernel<<<blocks_for(c), kBlock, 0, st>>>(n, s, beta);
 }
 
 void launch_y_only(const DevNet& n, const DevState& s, cudaStream_t st) {
-    if (n.m > 0) y_only_kernel<<<blocks_for(n.m), kBlock, 0, st>>>(n, s);
+    const int c = n.rows_count();
+    if (c > 0) y_only_kernel<<<blocks_for(c), kBlock, 0, st>>>(n, s);
 }
 
 void launch_outer(const DevNet& n, const DevState& s, double beta, double lmin, double lmax,
                   cudaStream_t st) {
-    if (n.m > 0) outer_kernel<<<blocks_for(n.m), kBlock, 0, st>>>(n, s, beta, lmin, lmax);
+    const int c = n.rows_count();
+    if (c > 0) outer_kernel<<<blocks_for(c), kBlock, 0, st>>>(n, s, beta, lmin, lmax);
 }
 
 void launch_clamp_gen_p(const DevNet& n, const DevState& s, cudaStream_t st) {
-    if (n.ng > 0) clamp_gen_p_kernel<<<blocks_for(n.ng), kBlock, 0, st>>>(n, s);
+    const int c = n.gens_count();
+    if (c > 0) clamp_gen_p_kernel<<<blocks_for(c), kBlock, 0, st>>>(n, s);
+}
+
+// dst[rows[t]] = src[rows[t]] for t < count (device-to-device, same device
+// or peer-mapped): boundary exchange of the in-process multi-part transport.
+__global__ void copy_rows_kernel(const int* rows, int count, const double* src, double* dst) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < count) dst[rows[t]] = src[rows[t]];
+}
+
+void launch_copy_rows(const int* rows, int count, const double* src, double* dst,
+                      cudaStream_t st) {
+    if (count > 0) copy_rows_kernel<<<blocks_for(count), kBlock, 0, st>>>(rows, count, src, dst);
+}
+
+// buf[t] = v[rows[t]] / v[rows[t]] = buf[t]: pack / unpack for NCCL.
+__global__ void gather_rows_kernel(const int* rows, int count, const double* v, double* buf) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < count) buf[t] = v[rows[t]];
+}
+__global__ void scatter_rows_kernel(const int* rows, int count, const double* buf, double* v) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < count) v[rows[t]] = buf[t];
+}
+
+void launch_gather_rows(const int* rows, int count, const double* v, double* buf,
+                        cudaStream_t st) {
+    if (count > 0) gather_rows_kernel<<<blocks_for(count), kBlock, 0, st>>>(rows, count, v, buf);
+}
+void launch_scatter_rows(const int* rows, int count, const double* buf, double* v,
+                         cudaStream_t st) {
+    if (count > 0) scatter_rows_kernel<<<blocks_for(count), kBlock, 0, st>>>(rows, count, buf, v);
 }
 
 void launch_rowmax(const double* v, int n, unsigned long long* dst, cudaStream_t st) {

@@ -28,7 +28,9 @@ double SolverConfig::effective_inner_tol(int m) const {
     return inner_tol > 0.0 ? inner_tol : eps * std::sqrt(static_cast<double>(m));
 }
 
-Session::Session(const Network& net, const SolverConfig& cfg) : net_(net), cfg_(cfg) {
+Session::Session(const Network& net, const SolverConfig& cfg, const PartPlan* plan)
+    : net_(net), cfg_(cfg) {
+    if (plan) plan_ = *plan;
     check(cudaSetDevice(cfg.device), "cudaSetDevice");
     check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
     for (auto& e : ev_) check(cudaEventCreate(&e), "cudaEventCreate");
@@ -108,6 +110,10 @@ void Session::upload_network() {
         for (int k = 0; k < 8; ++k) yc[static_cast<size_t>(k) * nl + b] = l.y.c[k];
         (l.limited() ? lim : unl).push_back(b);
     }
+    if (plan_.parts > 1) {  // this part solves only its own branches
+        lim = plan_.lim;
+        unl = plan_.unl;
+    }
     alloc(dn_.br_from, nl); put(dn_.br_from, from);
     alloc(dn_.br_to, nl); put(dn_.br_to, to);
     alloc(dn_.br_y, 8 * static_cast<size_t>(nl)); put(dn_.br_y, yc);
@@ -147,6 +153,20 @@ void Session::upload_network() {
     alloc(ds_.mig_iter, nl);
     alloc(ds_.mig_al, nl);
     alloc(ds_.mig_cost, nl);
+    if (plan_.parts > 1) {
+        alloc(dn_.own_gens, plan_.gens.size()); put(dn_.own_gens, plan_.gens);
+        alloc(dn_.own_buses, plan_.buses.size()); put(dn_.own_buses, plan_.buses);
+        alloc(dn_.own_rows, plan_.rows.size()); put(dn_.own_rows, plan_.rows);
+        dn_.n_own_gens = static_cast<int>(plan_.gens.size());
+        dn_.n_own_buses = static_cast<int>(plan_.buses.size());
+        dn_.n_own_rows = static_cast<int>(plan_.rows.size());
+        d_send_.assign(plan_.parts, nullptr);
+        d_recv_.assign(plan_.parts, nullptr);
+        for (int q = 0; q < plan_.parts; ++q) {
+            alloc(d_send_[q], plan_.send_x[q].size()); put(d_send_[q], plan_.send_x[q]);
+            alloc(d_recv_[q], plan_.recv_x[q].size()); put(d_recv_[q], plan_.recv_x[q]);
+        }
+    }
 }
 
 // make_state + cold_start (decomp.cpp:37-57, driver.cpp:26-63), on the host
@@ -339,7 +359,7 @@ int Session::timed_steps(int k, size_t flush_bytes, double* step_ms, double* rec
         if (flush_bytes) check(cudaMemsetAsync(flush_buf_, done & 0xff, flush_bytes, stream_), "flush");
         cudaEventRecord(a, stream_);
         double nrm[4];
-        const int fails = iterate(nrm, nullptr, b);
+        const int fails = iterate_ev(nrm, nullptr, b);
         float ms = 0.0f;
         cudaEventElapsedTime(&ms, a, b);
         if (step_ms) step_ms[done] = ms;
@@ -353,7 +373,8 @@ int Session::timed_steps(int k, size_t flush_bytes, double* step_ms, double* rec
     return done;
 }
 
-int Session::iterate(double out[4], PhaseTimes* times, cudaEvent_t end_event) {
+int Session::iterate_ev(double out[4], PhaseTimes* times, cudaEvent_t end_event) {
+    check(cudaSetDevice(cfg_.device), "cudaSetDevice");
     launch_reset_scalars(sc_, stream_);
     cudaEventRecord(ev_[0], stream_);
     launch_generators(dn_, ds_, stream_);
@@ -392,7 +413,37 @@ int Session::iterate(double out[4], PhaseTimes* times, cudaEvent_t end_event) {
     return static_cast<int>(h.failures);
 }
 
+void Session::enqueue_x_phase() {
+    check(cudaSetDevice(cfg_.device), "cudaSetDevice");
+    launch_reset_scalars(sc_, stream_);
+    launch_generators(dn_, ds_, stream_);
+    launch_branches(dn_, ds_, branch_cfg(cfg_), sc_, stream_);
+    check(cudaGetLastError(), "x phase launch");
+}
+
+void Session::enqueue_xbar_zy_phase() {
+    check(cudaSetDevice(cfg_.device), "cudaSetDevice");
+    launch_buses(dn_, ds_, sc_, stream_);
+    launch_zy(dn_, ds_, beta_, sc_, stream_);
+    check(cudaGetLastError(), "xbar/zy phase launch");
+    check(cudaMemcpyAsync(sc_host_, sc_, sizeof(DevScalars), cudaMemcpyDeviceToHost, stream_), "D2H");
+}
+
+IterScalars Session::read_scalars() {
+    check(cudaStreamSynchronize(stream_), "iteration sync");
+    const DevScalars& h = *sc_host_;
+    IterScalars r;
+    r.primal = from_bits(h.primal_inf);
+    r.dual_raw = from_bits(h.dual_inf);
+    r.z_inf = from_bits(h.z_inf);
+    r.z_drift = from_bits(h.z_drift);
+    r.failures = static_cast<int>(h.failures);
+    r.singular_bus = h.singular_bus == INT32_MAX ? -1 : h.singular_bus;
+    return r;
+}
+
 void Session::outer_update() {
+    check(cudaSetDevice(cfg_.device), "cudaSetDevice");
     launch_outer(dn_, ds_, beta_, cfg_.lambda_min, cfg_.lambda_max, stream_);
     check(cudaGetLastError(), "outer launch");
 }

@@ -114,7 +114,7 @@ QualityMetrics evaluate_solution(const Network& net, const Solution& sol) {
 
 namespace {
 
-void finish_report(Session& s, SolveReport& rep) {
+void finish_report(Engine& s, SolveReport& rep) {
     std::vector<double> gen_rows, w, th;
     s.download_solution_inputs(gen_rows, w, th);
     rep.solution = extract_solution(s.network(), gen_rows, w, th);
@@ -124,7 +124,7 @@ void finish_report(Session& s, SolveReport& rep) {
 }  // namespace
 
 // driver.cpp:140-246.  warm == false -> cold start on the device state.
-SolveReport solve(Session& s, const SolverConfig& cfg, bool warm) {
+SolveReport solve(Engine& s, const SolverConfig& cfg, bool warm) {
     const auto t0 = Clock::now();
     if (!warm) s.cold_start();
     SolveReport report;
@@ -179,7 +179,8 @@ std::vector<PeriodReport> run_tracking(const Network& net, const SolverConfig& c
             throw std::invalid_argument("per-bus multiplier row size mismatch");
     std::vector<PeriodReport> reports;
     reports.reserve(sc.periods());
-    Session session(net, cfg);
+    std::unique_ptr<Engine> eng = make_engine(net, cfg);
+    Engine& session = *eng;
     std::vector<double> prev_pg;
     const int nb = net.nb(), ng = net.ng();
     std::vector<double> pd(nb), qd(nb), pmin(ng), pmax(ng);

@@ -11,12 +11,14 @@
 #ifndef GA_SOLVER_HPP
 #define GA_SOLVER_HPP
 
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "device.hpp"
 #include "network.hpp"
+#include "partition.hpp"
 
 namespace ga {
 
@@ -39,6 +41,8 @@ struct SolverConfig {  // proj/src/driver.hpp:15-40
     BranchCfg tron;  // gtol, max_iterations, cg_tol, max_cg, delta_floor
     int workers = 1;  // accepted for API compatibility; unused on the GPU
     int device = 0;
+    int partitions = 1;  // bus-graph parts (multi.cpp); 1 = single session
+    int devices = 1;     // parts are placed round-robin on devices [device, device+devices)
 
     double effective_inner_tol(int m) const;
 };
@@ -98,27 +102,76 @@ struct KernelClock {
     long long launches = 0;
 };
 
-class Session {
+struct IterScalars {
+    double primal = 0, dual_raw = 0, z_inf = 0, z_drift = 0;
+    int failures = 0;
+    int singular_bus = -1;  // internal index of the first singular bus, -1 if none
+};
+
+// What the Algorithm-1 driver (solve, run_tracking) needs from a device
+// backend: one Session (one GPU), or MultiPart (a bus-graph partition over
+// several sessions with boundary exchange, multi.cpp).
+class Engine {
 public:
-    Session(const Network& net, const SolverConfig& cfg);
-    ~Session();
+    virtual ~Engine() = default;
+    virtual const Network& network() const = 0;
+    virtual const SolverConfig& config() const = 0;
+    virtual int m() const = 0;
+    virtual void cold_start() = 0;
+    virtual void upload_state(const HostState& s) = 0;
+    virtual void download_state(HostState& s) const = 0;
+    virtual double beta() const = 0;
+    virtual void set_beta(double b) = 0;
+    virtual void set_loads(const std::vector<double>& pd, const std::vector<double>& qd) = 0;
+    virtual void set_gen_p_bounds(const std::vector<double>& pmin,
+                                  const std::vector<double>& pmax) = 0;
+    virtual void clamp_gen_p() = 0;
+    // One inner iteration; out = primal, dual (raw), z_inf, z_drift; returns
+    // branch failures; throws SingularBusError.
+    virtual int iterate(double out[4], PhaseTimes* times) = 0;
+    virtual void outer_update() = 0;
+    virtual double rho_max() = 0;
+    virtual void download_solution_inputs(std::vector<double>& gen_rows, std::vector<double>& w,
+                                          std::vector<double>& th) const = 0;
+    virtual int parts() const { return 1; }
+};
+
+class Session : public Engine {
+public:
+    // plan == nullptr: the session owns the whole network; otherwise only the
+    // plan's generators / branches / buses / rows (multi-part runs).
+    Session(const Network& net, const SolverConfig& cfg, const PartPlan* plan = nullptr);
+    ~Session() override;
+
+    // Split inner iteration for multi-part drivers: x phase (generators +
+    // branches), bus + z/y phase, then the D2H of this part's scalars.
+    void enqueue_x_phase();
+    void enqueue_xbar_zy_phase();
+    IterScalars read_scalars();
+    cudaStream_t stream() const { return stream_; }
+    const DevState& dev_state() const { return ds_; }
+    const PartPlan* plan() const { return plan_.parts > 1 ? &plan_ : nullptr; }
+    // device copies of plan_.send_x[q] / recv_x[q]
+    const int* d_send_x(int q) const { return d_send_[q]; }
+    const int* d_recv_x(int q) const { return d_recv_[q]; }
     Session(const Session&) = delete;
     Session& operator=(const Session&) = delete;
 
-    const Network& network() const { return net_; }
-    const SolverConfig& config() const { return cfg_; }
-    int m() const { return dn_.m; }
+    const Network& network() const override { return net_; }
+    const SolverConfig& config() const override { return cfg_; }
+    int m() const override { return dn_.m; }
 
-    void cold_start();                      // driver.cpp:26-63 (host) -> upload
-    void upload_state(const HostState& s);  // any empty vector is skipped
-    void download_state(HostState& s) const;
-    double beta() const { return beta_; }
-    void set_beta(double b) { beta_ = b; }
+    void cold_start() override;                      // driver.cpp:26-63 (host) -> upload
+    void upload_state(const HostState& s) override;  // any empty vector is skipped
+    void download_state(HostState& s) const override;
+    double beta() const override { return beta_; }
+    void set_beta(double b) override { beta_ = b; }
 
     // Tracking: per-period loads and generator p-bounds (tracking.cpp:14-26,50-63).
-    void set_loads(const std::vector<double>& pd, const std::vector<double>& qd);
-    void set_gen_p_bounds(const std::vector<double>& pmin, const std::vector<double>& pmax);
-    void clamp_gen_p();
+    void set_loads(const std::vector<double>& pd, const std::vector<double>& qd) override;
+    void set_gen_p_bounds(const std::vector<double>& pmin,
+                          const std::vector<double>& pmax) override;
+    void clamp_gen_p() override;
 
     // One phase (phase-replay API).  Returns failures / singular bus / 0.
     long run_phase(int phase, double z_inf, double prev_z_inf);
@@ -127,15 +180,16 @@ public:
     // the scalars.  Fills out[0..3] = primal_inf, dual_inf (raw, before
     // rho_max), z_inf, z_drift; returns branch failures; throws
     // SingularBusError.
-    int iterate(double out[4], PhaseTimes* times, cudaEvent_t end_event = nullptr);
+    int iterate(double out[4], PhaseTimes* times) override { return iterate_ev(out, times, nullptr); }
+    int iterate_ev(double out[4], PhaseTimes* times, cudaEvent_t end_event);
 
     // Benchmark helper: k iterations, each bracketed by CUDA events on the
     // session stream (launches through the D2H of its norms); an L2 flush of
     // flush_bytes runs between steps outside the brackets.  records gets 5
     // doubles per step (primal, dual, z, z_drift, failures).
     int timed_steps(int k, size_t flush_bytes, double* step_ms, double* records);
-    void outer_update();                       // lambda clamp on the device
-    double rho_max();                          // max over rows, device reduction
+    void outer_update() override;              // lambda clamp on the device
+    double rho_max() override;                 // max over rows, device reduction
 
     KernelClock kernel_clock(int cls) const { return clocks_[cls]; }
     long long tron_iterations() const;
@@ -147,7 +201,7 @@ public:
 
     // Solution extraction inputs: x gen rows, bus_w, bus_theta.
     void download_solution_inputs(std::vector<double>& gen_rows, std::vector<double>& w,
-                                  std::vector<double>& th) const;
+                                  std::vector<double>& th) const override;
 
 private:
     void upload_network();
@@ -166,9 +220,15 @@ private:
     cudaEvent_t ev_[5] = {};
     KernelClock clocks_[4];
     std::vector<void*> allocs_;
+    PartPlan plan_;
+    std::vector<int*> d_send_, d_recv_;
 };
 
-SolveReport solve(Session& s, const SolverConfig& cfg, bool warm);
+SolveReport solve(Engine& s, const SolverConfig& cfg, bool warm);
+
+// One Session, or a MultiPart over cfg.partitions parts on cfg.devices
+// devices when partitions > 1 (multi.cpp).
+std::unique_ptr<Engine> make_engine(const Network& net, const SolverConfig& cfg);
 
 Solution extract_solution(const Network& net, const std::vector<double>& gen_rows,
                           const std::vector<double>& bus_w, const std::vector<double>& bus_theta);

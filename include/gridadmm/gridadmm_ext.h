@@ -84,6 +84,21 @@ gridadmm_status gridadmm_session_new(const gridadmm_network* net,
                                      gridadmm_session** out);
 void gridadmm_session_free(gridadmm_session* s);
 
+/* Multi-process bus-graph partition (one process per GPU, e.g. torchrun):
+ * rank 0 creates a 128-byte NCCL unique id, shares it out of band, and every
+ * rank opens its part on its configured `device`.  Rank r owns part r of
+ * gridadmm_network_partition(net, world); per inner iteration boundary rows
+ * and residual maxima go over NCCL (grouped send/recv, all-reduce), so every
+ * rank sees the same residual series as a 1-GPU solve.  Supported on such
+ * sessions: gridadmm_session_iterate (and _free); state getters return only
+ * the entries this rank owns as current.  NCCL (libnccl.so.2) is loaded at
+ * run time. */
+gridadmm_status gridadmm_nccl_unique_id(unsigned char* out);
+gridadmm_status gridadmm_session_new_dist(const gridadmm_network* net,
+                                          const gridadmm_config* cfg, int rank,
+                                          int world, const unsigned char* nccl_id,
+                                          gridadmm_session** out);
+
 /* Copies the device state to/from host arrays (synchronous). */
 gridadmm_status gridadmm_session_get_state(const gridadmm_session* s,
                                            const gridadmm_state_view* v);

@@ -81,6 +81,8 @@ EXT_SYMBOLS = {
     "gridadmm_network_partition": (_I, [_P, _I, _IP]),
     "gridadmm_session_new": (_I, [_P, _P, ctypes.POINTER(_P)]),
     "gridadmm_session_free": (None, [_P]),
+    "gridadmm_nccl_unique_id": (_I, [ctypes.c_char_p]),
+    "gridadmm_session_new_dist": (_I, [_P, _P, _I, _I, ctypes.c_char_p, ctypes.POINTER(_P)]),
     "gridadmm_session_get_state": (_I, [_P, ctypes.POINTER(StateView)]),
     "gridadmm_session_set_state": (_I, [_P, ctypes.POINTER(StateView)]),
     "gridadmm_session_phase": (_I, [_P, _I, _DP]),
@@ -358,11 +360,20 @@ def make_view(arrays: Dict[str, np.ndarray]) -> StateView:
 class Session:
     """Device-resident solver state (gridadmm_ext.h): phase replay + bench."""
 
-    def __init__(self, net: Network, cfg: Config):
-        h = _P()
-        _check(lib().gridadmm_session_new(net.handle, cfg.handle, ctypes.byref(h)))
+    def __init__(self, net: Network, cfg: Config, _handle=None):
+        h = _handle if _handle is not None else _P()
+        if _handle is None:
+            _check(lib().gridadmm_session_new(net.handle, cfg.handle, ctypes.byref(h)))
         self._h = h
         self.shapes = state_shapes(net.num_buses, net.num_generators, net.num_branches)
+
+    @classmethod
+    def distributed(cls, net: Network, cfg: Config, rank: int, world: int, nccl_id: bytes):
+        """Rank `rank` of a `world`-process bus-graph partition (NCCL exchange)."""
+        h = _P()
+        _check(lib().gridadmm_session_new_dist(net.handle, cfg.handle, rank, world, nccl_id,
+                                               ctypes.byref(h)))
+        return cls(net, cfg, _handle=h)
 
     def get_state(self) -> Dict[str, np.ndarray]:
         arrs = {k: np.zeros(n) for k, n in self.shapes.items()}
@@ -426,6 +437,12 @@ class Session:
             self._h = None
 
     __del__ = close
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().gridadmm_nccl_unique_id(buf))
+    return buf.raw
 
 
 def device_count() -> int:

@@ -388,6 +388,28 @@ gridadmm_status gridadmm_session_new(const gridadmm_network* net, const gridadmm
 
 void gridadmm_session_free(gridadmm_session* s) { delete s; }
 
+gridadmm_status gridadmm_nccl_unique_id(unsigned char* out) {
+    if (!out) return fail(GRIDADMM_ERR_INVALID_ARG, "null argument to nccl_unique_id");
+    return guarded([&]() -> gridadmm_status {
+        ga::nccl_unique_id(out);
+        return GRIDADMM_OK;
+    });
+}
+
+gridadmm_status gridadmm_session_new_dist(const gridadmm_network* net, const gridadmm_config* cfg,
+                                          int rank, int world, const unsigned char* nccl_id,
+                                          gridadmm_session** out) {
+    if (!net || !cfg || !out || !nccl_id || world < 1 || rank < 0 || rank >= world)
+        return fail(GRIDADMM_ERR_INVALID_ARG, "bad argument to session_new_dist");
+    return guarded([&]() -> gridadmm_status {
+        auto h = std::make_unique<gridadmm_session>();
+        h->e = ga::make_dist_engine(net->net, cfg->solver, rank, world, nccl_id);
+        h->e->cold_start();
+        *out = h.release();
+        return GRIDADMM_OK;
+    });
+}
+
 gridadmm_status gridadmm_session_get_state(const gridadmm_session* s, const gridadmm_state_view* v) {
     if (!s || !v) return fail(GRIDADMM_ERR_INVALID_ARG, "null argument to session_get_state");
     return guarded([&]() -> gridadmm_status {
@@ -467,9 +489,8 @@ gridadmm_status gridadmm_session_iterate(gridadmm_session* s, int n, double* rec
 gridadmm_status gridadmm_session_timed_steps(gridadmm_session* s, int n, size_t flush_bytes,
                                              double* step_ms, double* records) {
     if (!s || n < 0) return fail(GRIDADMM_ERR_INVALID_ARG, "bad argument to session_timed_steps");
-    if (!s->s) return fail(GRIDADMM_ERR_INVALID_ARG, "timed_steps needs a single-part session");
     return guarded([&]() -> gridadmm_status {
-        s->s->timed_steps(n, flush_bytes, step_ms, records);
+        s->e->timed_steps(n, flush_bytes, step_ms, records);
         return GRIDADMM_OK;
     });
 }

@@ -14,6 +14,7 @@
 // translation; only owned entries are computed.  Results are bit-identical
 // to one Session (tests/test_gpu_parity.py::test_partitioned_*).
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cstring>
 
@@ -177,6 +178,25 @@ public:
             for (int g : plans_[p].gens) { gen_rows[2 * g] = g2[2 * g]; gen_rows[2 * g + 1] = g2[2 * g + 1]; }
             for (int i : plans_[p].buses) { w[i] = w2[i]; th[i] = t2[i]; }
         }
+    }
+
+    int timed_steps(int k, size_t, double* step_ms, double* records) override {
+        // parts run on several streams: time each step host-side around the
+        // fully synchronous iterate (every step ends with all streams synced)
+        const double rmax = rho_max();
+        for (int i = 0; i < k; ++i) {
+            const auto t0 = std::chrono::steady_clock::now();
+            double nrm[4];
+            const int fails = iterate(nrm, nullptr);
+            const double ms = std::chrono::duration<double, std::milli>(
+                                  std::chrono::steady_clock::now() - t0).count();
+            if (step_ms) step_ms[i] = ms;
+            if (records) {
+                double* r = records + 5 * i;
+                r[0] = nrm[0]; r[1] = nrm[1] * rmax; r[2] = nrm[2]; r[3] = nrm[3]; r[4] = fails;
+            }
+        }
+        return k;
     }
 
     const std::vector<int>& part_of_bus() const { return part_of_bus_; }

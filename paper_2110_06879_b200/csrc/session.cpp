@@ -421,11 +421,15 @@ void Session::enqueue_x_phase() {
     check(cudaGetLastError(), "x phase launch");
 }
 
-void Session::enqueue_xbar_zy_phase() {
+void Session::enqueue_xbar_zy_phase(bool copy_scalars) {
     check(cudaSetDevice(cfg_.device), "cudaSetDevice");
     launch_buses(dn_, ds_, sc_, stream_);
     launch_zy(dn_, ds_, beta_, sc_, stream_);
     check(cudaGetLastError(), "xbar/zy phase launch");
+    if (copy_scalars) enqueue_scalars_d2h();
+}
+
+void Session::enqueue_scalars_d2h() {
     check(cudaMemcpyAsync(sc_host_, sc_, sizeof(DevScalars), cudaMemcpyDeviceToHost, stream_), "D2H");
 }
 

@@ -134,6 +134,8 @@ public:
     virtual void download_solution_inputs(std::vector<double>& gen_rows, std::vector<double>& w,
                                           std::vector<double>& th) const = 0;
     virtual int parts() const { return 1; }
+    // k iterations each bracketed by CUDA events (see Session::timed_steps)
+    virtual int timed_steps(int k, size_t flush_bytes, double* step_ms, double* records) = 0;
 };
 
 class Session : public Engine {
@@ -146,8 +148,10 @@ public:
     // Split inner iteration for multi-part drivers: x phase (generators +
     // branches), bus + z/y phase, then the D2H of this part's scalars.
     void enqueue_x_phase();
-    void enqueue_xbar_zy_phase();
+    void enqueue_xbar_zy_phase(bool copy_scalars = true);
+    void enqueue_scalars_d2h();
     IterScalars read_scalars();
+    DevScalars* dev_scalars() const { return sc_; }
     cudaStream_t stream() const { return stream_; }
     const DevState& dev_state() const { return ds_; }
     const PartPlan* plan() const { return plan_.parts > 1 ? &plan_ : nullptr; }
@@ -187,7 +191,7 @@ public:
     // session stream (launches through the D2H of its norms); an L2 flush of
     // flush_bytes runs between steps outside the brackets.  records gets 5
     // doubles per step (primal, dual, z, z_drift, failures).
-    int timed_steps(int k, size_t flush_bytes, double* step_ms, double* records);
+    int timed_steps(int k, size_t flush_bytes, double* step_ms, double* records) override;
     void outer_update() override;              // lambda clamp on the device
     double rho_max() override;                 // max over rows, device reduction
 
@@ -229,6 +233,12 @@ SolveReport solve(Engine& s, const SolverConfig& cfg, bool warm);
 // One Session, or a MultiPart over cfg.partitions parts on cfg.devices
 // devices when partitions > 1 (multi.cpp).
 std::unique_ptr<Engine> make_engine(const Network& net, const SolverConfig& cfg);
+
+// One process per GPU (dist.cpp): rank `rank` of `world` owns part rank of
+// partition_buses(net, world); boundary rows and norms go over NCCL.
+void nccl_unique_id(unsigned char out[128]);
+std::unique_ptr<Engine> make_dist_engine(const Network& net, const SolverConfig& cfg, int rank,
+                                         int world, const unsigned char* id);
 
 Solution extract_solution(const Network& net, const std::vector<double>& gen_rows,
                           const std::vector<double>& bus_w, const std::vector<double>& bus_theta);

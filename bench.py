@@ -287,7 +287,7 @@ def run_b200(args, d: Dist):
     cfg = ga.Config(args.preset, device=dev)
     nb, ng, nl, m = net.num_buses, net.num_generators, net.num_branches, net.num_rows
 
-    if d.world > 1:
+    if d.world > 1 or os.environ.get("GRIDADMM_BENCH_DIST") == "1":
         return run_b200_partitioned(args, d, ga, path, net)
 
     # --- device-resident timed region -----------------------------------

@@ -188,6 +188,49 @@ class RefNet:
         return series[: 6 * k].reshape(-1, 6), info, fin
 
 
+def ref_capi():
+    """The reference's own C ABI (the 23 gridadmm_* symbols of
+    proj/include/gridadmm/gridadmm.h) from _ref/libgridadmm_ref.so, typed like
+    the product binding so reports can be compared call for call."""
+    import paper_2110_06879_b200 as ga
+    h = RefLib.get()
+    for name, (res, args) in ga.SYMBOLS.items():
+        fn = getattr(h, name)
+        fn.restype = res
+        fn.argtypes = args
+    return h
+
+
+def ref_track(case_path: str, profile_csv: str, preset: str, **cfg):
+    """gridadmm_track_run through the reference's C ABI; returns a list of
+    per-period metric dicts and the status."""
+    import paper_2110_06879_b200 as ga
+    h = ref_capi()
+    net = ctypes.c_void_p()
+    assert h.gridadmm_network_load(os.fsencode(case_path), ctypes.byref(net)) == 0
+    c = h.gridadmm_config_new()
+    assert h.gridadmm_config_preset(c, preset.encode()) == 0
+    for k, v in cfg.items():
+        assert h.gridadmm_config_set(c, k.encode(), float(v)) == 0, k
+    trk = ctypes.c_void_p()
+    st = h.gridadmm_track_run(net, c, os.fsencode(profile_csv), ctypes.byref(trk))
+    out = []
+    for p in range(1, h.gridadmm_track_num_periods(trk) + 1):
+        rep = ctypes.c_void_p()
+        assert h.gridadmm_track_period_report(trk, p, ctypes.byref(rep)) == 0
+        m = {}
+        for key in ga.METRIC_KEYS:
+            v = ctypes.c_double()
+            h.gridadmm_report_metric(rep, key.encode(), ctypes.byref(v))
+            m[key] = v.value
+        out.append(m)
+        h.gridadmm_report_free(rep)
+    h.gridadmm_track_free(trk)
+    h.gridadmm_config_free(c)
+    h.gridadmm_network_free(net)
+    return st, out
+
+
 class OracleNet(ctypes.Structure):
     _fields_ = [("nb", ctypes.c_int), ("ng", ctypes.c_int), ("nl", ctypes.c_int),
                 ("ref_bus", ctypes.c_int), ("bus", _DP), ("gen", _DP), ("ends", _IP),

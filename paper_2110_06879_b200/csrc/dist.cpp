@@ -103,7 +103,7 @@ public:
         for (double* p : rbuf_) cudaFree(p);
     }
 
-    const Network& network() const override { return net_; }
+    const Network& network() const override { return sess_->network(); }  // period network
     const SolverConfig& config() const override { return cfg_; }
     int m() const override { return net_.m(); }
     int parts() const override { return world_; }

@@ -96,9 +96,17 @@ public:
     }
     void set_loads(const std::vector<double>& pd, const std::vector<double>& qd) override {
         for (auto& p : parts_) on(*p).set_loads(pd, qd);
+        for (size_t i = 0; i < pd.size(); ++i) {  // period network for the metrics
+            net_.buses[i].pd = pd[i];
+            net_.buses[i].qd = qd[i];
+        }
     }
     void set_gen_p_bounds(const std::vector<double>& a, const std::vector<double>& b) override {
         for (auto& p : parts_) on(*p).set_gen_p_bounds(a, b);
+        for (size_t g = 0; g < a.size(); ++g) {
+            net_.gens[g].pmin = a[g];
+            net_.gens[g].pmax = b[g];
+        }
     }
     void clamp_gen_p() override {
         for (auto& p : parts_) on(*p).clamp_gen_p();

@@ -290,6 +290,12 @@ void Session::set_loads(const std::vector<double>& pd, const std::vector<double>
     check(cudaMemcpyAsync(dn_.b_qd, qd.data(), qd.size() * sizeof(double), cudaMemcpyHostToDevice,
                           stream_), "set_loads");
     check(cudaStreamSynchronize(stream_), "sync");
+    // the host copy is the period network the quality metrics are evaluated
+    // on (tracking.cpp:47 scaled_network -> driver.cpp:89 evaluate_solution)
+    for (size_t i = 0; i < pd.size() && i < net_.buses.size(); ++i) {
+        net_.buses[i].pd = pd[i];
+        net_.buses[i].qd = qd[i];
+    }
 }
 
 void Session::set_gen_p_bounds(const std::vector<double>& pmin, const std::vector<double>& pmax) {
@@ -298,6 +304,10 @@ void Session::set_gen_p_bounds(const std::vector<double>& pmin, const std::vecto
     check(cudaMemcpyAsync(dn_.g_pmax, pmax.data(), pmax.size() * sizeof(double),
                           cudaMemcpyHostToDevice, stream_), "set_gen_p_bounds");
     check(cudaStreamSynchronize(stream_), "sync");
+    for (size_t g = 0; g < pmin.size() && g < net_.gens.size(); ++g) {  // ramp window
+        net_.gens[g].pmin = pmin[g];
+        net_.gens[g].pmax = pmax[g];
+    }
 }
 
 void Session::clamp_gen_p() {

@@ -60,7 +60,10 @@ constexpr double kRhoTildeMax = 1e7;
 
 constexpr int kLaneBlock = 128;  // lane phase: one slot per thread
 constexpr int kTileBlock = 128;  // tile phase: one slot per tile
-constexpr int kTile = 8;         // lanes per branch in the tile phase
+#ifndef GA_TILE
+#define GA_TILE 8
+#endif
+constexpr int kTile = GA_TILE;   // lanes per branch in the tile phase
 constexpr int kCounters = 8;
 
 // Workspace: [overflow6 n_lim | overflow4 n_unl | counters]
@@ -150,7 +153,11 @@ __device__ __forceinline__ void finalize_branch(const DevNet& net, const DevStat
     xr[1] = make_double2(fl[2], fl[3]);
     xr[2] = make_double2(pt[0] * pt[0], pt[2]);
     xr[3] = make_double2(pt[1] * pt[1], pt[3]);
+#ifdef GA_TRON_STATS
+    (void)iters;  // stats build: br_cost = executed steps (+2^20 if the tile phase ran it)
+#else
     st.br_cost[b] = iters;
+#endif
 }
 
 // Solve-level status of a TRON step that did not continue; updates iters.
@@ -231,6 +238,9 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
                 const int status = solve_status<N, kLaneBlock, SerialSearch>(r, iter_before, p, ts,
                                                                             tp, iters);
                 const int act = al_after_solve<N>(status, slot, p, ts, al_it, prev_res);
+#ifdef GA_TRON_STATS
+                if (act != kAlContinue) st.br_cost[b] = steps + 1;
+#endif
                 if (act != kAlContinue) end_branch(act);
             }
             if (b >= 0 && ++steps >= cfg.lane_budget) {
@@ -246,6 +256,9 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
                 st.lt_ij[b] = slot(F_LTIJ);
                 st.lt_ji[b] = slot(F_LTJI);
                 st.rho_t[b] = slot(F_RHOT);
+#ifdef GA_TRON_STATS
+                st.br_cost[b] = steps;
+#endif
                 ovf[atomicAdd(ovf_count, 1)] = b;
                 b = -1;
             }
@@ -326,10 +339,12 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
         int iters = st.mig_cost[b];
         __syncwarp(mask);
         int act = kAlContinue;
+        unsigned branch_exec = 0;
         while (act == kAlContinue) {
             const int iter_before = ts.iter;
             const int r = tron_step<N>(p, ts, tp, search);
             ++my_exec;
+            ++branch_exec;
             if (r == kStepContinue) continue;
             const int status = solve_status<N, S, TileSearch<kTile>>(r, iter_before, p, ts, tp, iters);
             act = al_after_solve<N>(status, slot, p, ts, al_it, prev_res);
@@ -337,6 +352,9 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
         __syncwarp(mask);
         if (rank == 0) {
             finalize_branch<N>(net, st, slot, ts, b, act == kAlFailed, iters);
+#ifdef GA_TRON_STATS
+            st.br_cost[b] += (int)branch_exec + (1 << 20);
+#endif
             my_iters += iters;
             my_fail += act == kAlFailed ? 1 : 0;
         }

@@ -500,6 +500,273 @@ __global__ void __launch_bounds__(kBusWarps * 32) bus_warp_kernel(DevNet n, DevS
     block_max_atomic<1>(vals, dst);
 }
 
+// Block-staged bus kernel (the one launched), optionally fused with the z / y
+// updates and all four residual norms.
+//
+// The warp-per-bus kernel above spends its time issuing lane 0's serial code
+// (ncu: 4 active threads per warp, 59% issue-slot busy).  Here a block of
+// kBB threads owns kBB consecutive buses and works in three phases:
+//   1. gather: the block's rows (CSR, contiguous per bus) are spread over all
+//      threads; each thread loads rho, x, z, y of a row and stages either
+//      (rho, c) for the w / theta columns or the S / rhs terms (a*a/rho,
+//      a*c/rho) of a duplicate column (kernels.cpp:311-361) in shared memory;
+//   2. solve: thread = bus: the ordered sums, the NC x NC elimination and mu,
+//      with every lane of the warp busy;
+//   3. write: rows again spread over all threads: xbar = (c - A'mu)/rho
+//      (kernels.cpp:394-399) and, fused, z (kernels.cpp:415-422), y
+//      (kernels.cpp:424-428) and the primal / dual / z / drift maxima.
+// Fusing z / y is exact: every row is consumed by exactly one bus
+// (proj/tests/test_decomp.cpp:59-71) and z / y of a row depend only on that
+// row, so the order "all buses, then all z, then all y" is not observable.
+constexpr int kBB = 128;
+constexpr int kStage = 2048;  // staged rows per block; the rest are read from global
+
+// largest slot with off[slot] <= p  (off[0] = 0 <= p < off[kBB])
+__device__ __forceinline__ int find_slot(const int* off, int p) {
+    int lo = 0, hi = kBB;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (off[mid] <= p) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// column group of local row k: 0 w, 1 theta, 2 gen_p, 3 gen_q, 4 flow_p, 5 flow_q
+__device__ __forceinline__ int group_of(const int* gl, int k) {
+    int g = 0;
+#pragma unroll
+    for (int j = 1; j < 6; ++j) g += k >= gl[j] ? 1 : 0;
+    return g;
+}
+
+constexpr int kFlagNonfinite = 1, kFlagSingular = 2, kFlagRef = 4;
+
+template <bool kZY>
+__global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, double beta,
+                                                       DevScalars* sc) {
+    __shared__ int s_off[kBB + 1];
+    __shared__ int s_base[kBB];
+    __shared__ int s_gl[kBB][8];  // local group offsets 0..6, [7] = flags
+    __shared__ double s_res[kBB][5];  // mu0..2, w, theta
+    __shared__ double s_a[kStage], s_b[kStage];
+    __shared__ int s_wsum[kBB / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int t = blockIdx.x * kBB + tid;
+    const int nbus = n.buses_count();
+    int i = -1, cnt = 0;
+    {
+        int gl[7] = {0, 0, 0, 0, 0, 0, 0}, g0 = 0;
+        if (t < nbus) {
+            i = n.bus_at(t);
+            const int* grp = n.bus_grp + 7 * i;
+            g0 = grp[0];
+#pragma unroll
+            for (int k = 0; k < 7; ++k) gl[k] = grp[k] - g0;
+            cnt = gl[6];
+        }
+        s_base[tid] = g0;
+#pragma unroll
+        for (int k = 0; k < 7; ++k) s_gl[tid][k] = gl[k];
+        s_gl[tid][7] = (i >= 0 && i == n.ref_bus) ? kFlagRef : 0;
+    }
+    // block exclusive scan of the row counts
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) s_wsum[wid] = incl;
+    __syncthreads();
+    int woff = 0;
+#pragma unroll
+    for (int w = 0; w < kBB / 32; ++w) woff += w < wid ? s_wsum[w] : 0;
+    s_off[tid] = woff + incl - cnt;
+    if (tid == kBB - 1) s_off[kBB] = woff + incl;
+    __syncthreads();
+    const int total = s_off[kBB];
+    const int staged = total < kStage ? total : kStage;
+
+    // 1. gather
+    for (int p = tid; p < staged; p += kBB) {
+        const int slot = find_slot(s_off, p);
+        const int k = p - s_off[slot];
+        const int row = n.bus_rows[s_base[slot] + k];
+        const double q = s.rho[row];
+        const double c = q * (s.x[row] + s.z[row]) + s.y[row];
+        const int g = group_of(s_gl[slot], k);
+        if (g < 2) {
+            s_a[p] = q;
+            s_b[p] = c;
+        } else {
+            if (!sfinite(c)) atomicOr(&s_gl[slot][7], kFlagNonfinite);
+            const double a = g < 4 ? 1.0 : -1.0;  // gen columns +1, flow columns -1
+            s_a[p] = a * a / q;
+            s_b[p] = a * c / q;
+        }
+    }
+    __syncthreads();
+
+    // 2. solve (thread = bus), kernels.cpp:303-391
+    if (i >= 0) {
+        const int base = s_off[tid];
+        int gl[7];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) gl[k] = s_gl[tid][k];
+        const int* rows = n.bus_rows + s_base[tid];
+        const bool ref = (s_gl[tid][7] & kFlagRef) != 0;
+        const int nc = ref ? 3 : 2;
+        const double gs = n.b_gs[i], bs = n.b_bs[i];
+        auto raw = [&](int k, double* q, double* c) {
+            const int row = rows[k];
+            *q = s.rho[row];
+            *c = *q * (s.x[row] + s.z[row]) + s.y[row];
+        };
+        auto staged_qc = [&](int k, double* q, double* c) {  // w / theta rows
+            const int p = base + k;
+            if (p < kStage) { *q = s_a[p]; *c = s_b[p]; }
+            else raw(k, q, c);
+        };
+        double q0 = 0.0, c0 = 0.0, q1 = 0.0, c1 = 0.0, q, c;
+        for (int k = 0; k < gl[1]; ++k) { staged_qc(k, &q, &c); q0 += q; c0 += c; }
+        for (int k = gl[1]; k < gl[2]; ++k) { staged_qc(k, &q, &c); q1 += q; c1 += c; }
+        if (q0 == 0.0) q0 = 1.0;
+        if (q1 == 0.0) q1 = 1.0;
+        bool finite = sfinite(c0) && sfinite(c1) && !(s_gl[tid][7] & kFlagNonfinite);
+        for (int k = max(gl[2], kStage - base); k < gl[6] && finite; ++k) {
+            raw(k, &q, &c);
+            finite = sfinite(c);
+        }
+        double S[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, rhs[3] = {0, 0, 0};
+        const double bvec[3] = {n.b_pd[i], n.b_qd[i], 0.0};
+        if (finite) {
+            const double a00 = -gs, a10 = bs;
+            double s00 = 0.0, s01 = 0.0, s11 = 0.0, s22 = 0.0, r0 = 0.0, r1 = 0.0, r2 = 0.0;
+            s00 += a00 * a00 / q0;
+            s01 += a00 * a10 / q0;
+            s11 += a10 * a10 / q0;
+            r0 += a00 * c0 / q0;
+            r1 += a10 * c0 / q0;
+            if (ref) {
+                s22 += 1.0 * 1.0 / q1;
+                r2 += 1.0 * c1 / q1;
+            }
+            auto term = [&](int k, double a, double* ts, double* tr) {
+                const int p = base + k;
+                if (p < kStage) { *ts = s_a[p]; *tr = s_b[p]; return; }
+                raw(k, &q, &c);
+                *ts = a * a / q;
+                *tr = a * c / q;
+            };
+            double ts, tr;
+            for (int k = gl[2]; k < gl[3]; ++k) { term(k, 1.0, &ts, &tr); s00 += ts; r0 += tr; }
+            for (int k = gl[4]; k < gl[5]; ++k) { term(k, -1.0, &ts, &tr); s00 += ts; r0 += tr; }
+            for (int k = gl[3]; k < gl[4]; ++k) { term(k, 1.0, &ts, &tr); s11 += ts; r1 += tr; }
+            for (int k = gl[5]; k < gl[6]; ++k) { term(k, -1.0, &ts, &tr); s11 += ts; r1 += tr; }
+            S[0] = s00; S[1] = s01; S[3] = s01; S[4] = s11;
+            S[8] = s22;
+            rhs[0] = r0 - bvec[0];
+            rhs[1] = r1 - bvec[1];
+            rhs[2] = r2 - bvec[2];
+        } else {
+            // dense reference loop (kernels.cpp:350-361), any column value
+            auto col = [&](int j, int* gg, double* qj, double* cj) {
+                if (j == 0) { *gg = 0; *qj = q0; *cj = c0; return; }
+                if (j == 1) { *gg = 1; *qj = q1; *cj = c1; return; }
+                const int k = gl[2] + (j - 2);
+                *gg = group_of(gl, k);
+                raw(k, qj, cj);
+            };
+            const int nv = 2 + (gl[6] - gl[2]);
+            for (int r = 0; r < nc; ++r) {
+                for (int t2 = 0; t2 < nc; ++t2) {
+                    double acc = 0.0;
+                    for (int j = 0; j < nv; ++j) {
+                        int gg; double qj, cj;
+                        col(j, &gg, &qj, &cj);
+                        acc += a_coef(r, gg, gs, bs, ref) * a_coef(t2, gg, gs, bs, ref) / qj;
+                    }
+                    S[r * 3 + t2] = acc;
+                }
+                double acc = 0.0;
+                for (int j = 0; j < nv; ++j) {
+                    int gg; double qj, cj;
+                    col(j, &gg, &qj, &cj);
+                    acc += a_coef(r, gg, gs, bs, ref) * cj / qj;
+                }
+                rhs[r] = acc - bvec[r];
+            }
+        }
+        double mu[3] = {0, 0, 0};
+        const bool singular = ref ? !ge_solve<3>(S, rhs, mu) : !ge_solve<2>(S, rhs, mu);
+        if (!singular) {
+            double acc = c0;
+            for (int r = 0; r < nc; ++r) acc -= a_coef(r, 0, gs, bs, ref) * mu[r];
+            const double w = acc / q0;
+            acc = c1;
+            for (int r = 0; r < nc; ++r) acc -= a_coef(r, 1, gs, bs, ref) * mu[r];
+            const double th = acc / q1;
+            s.bus_w[i] = w;
+            s.bus_theta[i] = th;
+            s_res[tid][3] = w;
+            s_res[tid][4] = th;
+        } else {
+            atomicMin(&sc->singular_bus, i);
+            s_gl[tid][7] |= kFlagSingular;
+        }
+        s_res[tid][0] = mu[0];
+        s_res[tid][1] = mu[1];
+        s_res[tid][2] = mu[2];
+    }
+    __syncthreads();
+
+    // 3. write xbar (+ z, y) and the norms
+    double dual = 0.0, pr = 0.0, zi = 0.0, zd = 0.0;
+    for (int p = tid; p < total; p += kBB) {
+        const int slot = find_slot(s_off, p);
+        const int k = p - s_off[slot];
+        const int row = n.bus_rows[s_base[slot] + k];
+        const int flags = s_gl[slot][7];
+        const double old = s.xbar[row];
+        const double q = s.rho[row], xv = s.x[row], zv = s.z[row], yv = s.y[row];
+        double xb = old;
+        if (!(flags & kFlagSingular)) {
+            const int g = group_of(s_gl[slot], k);
+            if (g == 0) xb = s_res[slot][3];
+            else if (g == 1) xb = s_res[slot][4];
+            else {
+                // a_coef(r, g >= 2) does not depend on gs / bs / ref
+                const int nc = (flags & kFlagRef) ? 3 : 2;
+                double acc = q * (xv + zv) + yv;
+                for (int r = 0; r < nc; ++r) acc -= a_coef(r, g, 0.0, 0.0, false) * s_res[slot][r];
+                xb = acc / q;
+            }
+            dual = smax(dual, abs_or_zero(xb - old));
+            s.xbar[row] = xb;
+        }
+        if (kZY) {
+            const double r = xv - xb;
+            const double z = -(s.lambda[row] + yv + q * r) / (q + beta);
+            const double res = xv - xb + z;
+            s.z[row] = z;
+            s.y[row] = yv + q * res;
+            pr = smax(pr, abs_or_zero(res));
+            zi = smax(zi, abs_or_zero(z));
+            zd = smax(zd, abs_or_zero(z - zv));
+        }
+    }
+    if (kZY) {
+        double vals[4] = {dual, pr, zi, zd};
+        unsigned long long* const dst[4] = {&sc->dual_inf, &sc->primal_inf, &sc->z_inf, &sc->z_drift};
+        block_max_atomic<4>(vals, dst);
+    } else {
+        double vals[1] = {dual};
+        unsigned long long* const dst[1] = {&sc->dual_inf};
+        block_max_atomic<1>(vals, dst);
+    }
+}
+
 // ---- fused z / y / residual (kernels.cpp:415-428, decomp.cpp:59-72) -----
 __global__ void __launch_bounds__(kBlock) zy_kernel(DevNet n, DevState s, double beta,
                                                     DevScalars* sc) {
@@ -649,6 +916,18 @@ void launch_generators(const DevNet& n, const DevState& s, cudaStream_t st) {
 }
 
 void launch_buses(const DevNet& n, const DevState& s, DevScalars* sc, cudaStream_t st) {
+    const int c = n.buses_count();
+    if (c > 0) bus_block_kernel<false><<<(c + kBB - 1) / kBB, kBB, 0, st>>>(n, s, 0.0, sc);
+}
+
+void launch_bus_zy(const DevNet& n, const DevState& s, double beta, DevScalars* sc,
+                   cudaStream_t st) {
+    const int c = n.buses_count();
+    if (c > 0) bus_block_kernel<true><<<(c + kBB - 1) / kBB, kBB, 0, st>>>(n, s, beta, sc);
+}
+
+// Warp-per-bus kernel (previous version, kept for A/B timing).
+void launch_buses_warp(const DevNet& n, const DevState& s, DevScalars* sc, cudaStream_t st) {
     const int c = n.buses_count();
     if (c <= 0) return;
     static int max_blocks = 0;

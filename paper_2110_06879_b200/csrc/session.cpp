@@ -391,9 +391,8 @@ int Session::iterate_ev(double out[4], PhaseTimes* times, cudaEvent_t end_event)
     cudaEventRecord(ev_[1], stream_);
     launch_branches(dn_, ds_, branch_cfg(cfg_), sc_, stream_);
     cudaEventRecord(ev_[2], stream_);
-    launch_buses(dn_, ds_, sc_, stream_);
+    launch_bus_zy(dn_, ds_, beta_, sc_, stream_);
     cudaEventRecord(ev_[3], stream_);
-    launch_zy(dn_, ds_, beta_, sc_, stream_);
     cudaEventRecord(ev_[4], stream_);
     check(cudaGetLastError(), "iteration launch");
     check(cudaMemcpyAsync(sc_host_, sc_, sizeof(DevScalars), cudaMemcpyDeviceToHost, stream_), "D2H");
@@ -433,8 +432,7 @@ void Session::enqueue_x_phase() {
 
 void Session::enqueue_xbar_zy_phase(bool copy_scalars) {
     check(cudaSetDevice(cfg_.device), "cudaSetDevice");
-    launch_buses(dn_, ds_, sc_, stream_);
-    launch_zy(dn_, ds_, beta_, sc_, stream_);
+    launch_bus_zy(dn_, ds_, beta_, sc_, stream_);
     check(cudaGetLastError(), "xbar/zy phase launch");
     if (copy_scalars) enqueue_scalars_d2h();
 }

@@ -550,19 +550,21 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
     __shared__ int s_gl[kBB][8];  // local group offsets 0..6, [7] = flags
     __shared__ double s_res[kBB][5];  // mu0..2, w, theta
     __shared__ double s_a[kStage], s_b[kStage];
+    __shared__ unsigned short s_pos[kStage];  // staged position -> slot << 3 | group
     __shared__ int s_wsum[kBB / 32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int t = blockIdx.x * kBB + tid;
     const int nbus = n.buses_count();
     int i = -1, cnt = 0;
+    int gl[7] = {0, 0, 0, 0, 0, 0, 0};
     {
-        int gl[7] = {0, 0, 0, 0, 0, 0, 0}, g0 = 0;
+        int g0 = 0;
         if (t < nbus) {
             i = n.bus_at(t);
             const int* grp = n.bus_grp + 7 * i;
-            g0 = grp[0];
+            g0 = __ldg(grp);
 #pragma unroll
-            for (int k = 0; k < 7; ++k) gl[k] = grp[k] - g0;
+            for (int k = 1; k < 7; ++k) gl[k] = __ldg(grp + k) - g0;
             cnt = gl[6];
         }
         s_base[tid] = g0;
@@ -582,38 +584,79 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
     int woff = 0;
 #pragma unroll
     for (int w = 0; w < kBB / 32; ++w) woff += w < wid ? s_wsum[w] : 0;
-    s_off[tid] = woff + incl - cnt;
+    const int my_off = woff + incl - cnt;
+    s_off[tid] = my_off;
     if (tid == kBB - 1) s_off[kBB] = woff + incl;
+    // position map of this bus's staged rows
+    {
+        int g = 0;
+        for (int k = 0; k < cnt && my_off + k < kStage; ++k) {
+            while (g < 5 && k >= gl[g + 1]) ++g;
+            s_pos[my_off + k] = static_cast<unsigned short>(tid << 3 | g);
+        }
+    }
     __syncthreads();
     const int total = s_off[kBB];
     const int staged = total < kStage ? total : kStage;
-
-    // 1. gather
-    for (int p = tid; p < staged; p += kBB) {
-        const int slot = find_slot(s_off, p);
-        const int k = p - s_off[slot];
-        const int row = n.bus_rows[s_base[slot] + k];
-        const double q = s.rho[row];
-        const double c = q * (s.x[row] + s.z[row]) + s.y[row];
-        const int g = group_of(s_gl[slot], k);
-        if (g < 2) {
-            s_a[p] = q;
-            s_b[p] = c;
+    // (slot, local row, group) of position p
+    auto locate = [&](int p, int* slot, int* k, int* g) {
+        if (p < kStage) {
+            const int v = s_pos[p];
+            *slot = v >> 3;
+            *g = v & 7;
         } else {
-            if (!sfinite(c)) atomicOr(&s_gl[slot][7], kFlagNonfinite);
-            const double a = g < 4 ? 1.0 : -1.0;  // gen columns +1, flow columns -1
-            s_a[p] = a * a / q;
-            s_b[p] = a * c / q;
+            *slot = find_slot(s_off, p);
+            *g = -1;
+        }
+        *k = p - s_off[*slot];
+        if (*g < 0) *g = group_of(s_gl[*slot], *k);
+    };
+
+    // 1. gather: kUnroll positions per thread per trip, loads issued together
+    constexpr int kUnroll = 4;
+    for (int p0 = tid; p0 < staged; p0 += kBB * kUnroll) {
+        int row[kUnroll], slot[kUnroll], g[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const int p = p0 + u * kBB;
+            row[u] = -1;
+            if (p < staged) {
+                int k;
+                locate(p, &slot[u], &k, &g[u]);
+                row[u] = __ldg(n.bus_rows + s_base[slot[u]] + k);
+            }
+        }
+        double q[kUnroll], xv[kUnroll], zv[kUnroll], yv[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            if (row[u] >= 0) {
+                q[u] = __ldg(s.rho + row[u]);
+                xv[u] = __ldg(s.x + row[u]);
+                zv[u] = __ldg(s.z + row[u]);
+                yv[u] = __ldg(s.y + row[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            if (row[u] < 0) continue;
+            const int p = p0 + u * kBB;
+            const double c = q[u] * (xv[u] + zv[u]) + yv[u];
+            if (g[u] < 2) {
+                s_a[p] = q[u];
+                s_b[p] = c;
+            } else {
+                if (!sfinite(c)) atomicOr(&s_gl[slot[u]][7], kFlagNonfinite);
+                const double a = g[u] < 4 ? 1.0 : -1.0;  // gen columns +1, flow columns -1
+                s_a[p] = a * a / q[u];
+                s_b[p] = a * c / q[u];
+            }
         }
     }
     __syncthreads();
 
     // 2. solve (thread = bus), kernels.cpp:303-391
     if (i >= 0) {
-        const int base = s_off[tid];
-        int gl[7];
-#pragma unroll
-        for (int k = 0; k < 7; ++k) gl[k] = s_gl[tid][k];
+        const int base = my_off;
         const int* rows = n.bus_rows + s_base[tid];
         const bool ref = (s_gl[tid][7] & kFlagRef) != 0;
         const int nc = ref ? 3 : 2;
@@ -721,39 +764,62 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
     }
     __syncthreads();
 
-    // 3. write xbar (+ z, y) and the norms
+    // 3. write xbar (+ z, y) and the norms; the old values read here were
+    // not written before in this kernel (each row belongs to one block)
     double dual = 0.0, pr = 0.0, zi = 0.0, zd = 0.0;
-    for (int p = tid; p < total; p += kBB) {
-        const int slot = find_slot(s_off, p);
-        const int k = p - s_off[slot];
-        const int row = n.bus_rows[s_base[slot] + k];
-        const int flags = s_gl[slot][7];
-        const double old = s.xbar[row];
-        const double q = s.rho[row], xv = s.x[row], zv = s.z[row], yv = s.y[row];
-        double xb = old;
-        if (!(flags & kFlagSingular)) {
-            const int g = group_of(s_gl[slot], k);
-            if (g == 0) xb = s_res[slot][3];
-            else if (g == 1) xb = s_res[slot][4];
-            else {
-                // a_coef(r, g >= 2) does not depend on gs / bs / ref
-                const int nc = (flags & kFlagRef) ? 3 : 2;
-                double acc = q * (xv + zv) + yv;
-                for (int r = 0; r < nc; ++r) acc -= a_coef(r, g, 0.0, 0.0, false) * s_res[slot][r];
-                xb = acc / q;
+    for (int p0 = tid; p0 < total; p0 += kBB * kUnroll) {
+        int row[kUnroll], slot[kUnroll], g[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const int p = p0 + u * kBB;
+            row[u] = -1;
+            if (p < total) {
+                int k;
+                locate(p, &slot[u], &k, &g[u]);
+                row[u] = __ldg(n.bus_rows + s_base[slot[u]] + k);
             }
-            dual = smax(dual, abs_or_zero(xb - old));
-            s.xbar[row] = xb;
         }
-        if (kZY) {
-            const double r = xv - xb;
-            const double z = -(s.lambda[row] + yv + q * r) / (q + beta);
-            const double res = xv - xb + z;
-            s.z[row] = z;
-            s.y[row] = yv + q * res;
-            pr = smax(pr, abs_or_zero(res));
-            zi = smax(zi, abs_or_zero(z));
-            zd = smax(zd, abs_or_zero(z - zv));
+        double old[kUnroll], q[kUnroll], xv[kUnroll], zv[kUnroll], yv[kUnroll], lam[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            if (row[u] >= 0) {
+                old[u] = __ldg(s.xbar + row[u]);
+                q[u] = __ldg(s.rho + row[u]);
+                xv[u] = __ldg(s.x + row[u]);
+                zv[u] = __ldg(s.z + row[u]);
+                yv[u] = __ldg(s.y + row[u]);
+                if (kZY) lam[u] = __ldg(s.lambda + row[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            if (row[u] < 0) continue;
+            const int flags = s_gl[slot[u]][7];
+            double xb = old[u];
+            if (!(flags & kFlagSingular)) {
+                if (g[u] == 0) xb = s_res[slot[u]][3];
+                else if (g[u] == 1) xb = s_res[slot[u]][4];
+                else {
+                    // a_coef(r, g >= 2) does not depend on gs / bs / ref
+                    const int nc = (flags & kFlagRef) ? 3 : 2;
+                    double acc = q[u] * (xv[u] + zv[u]) + yv[u];
+                    for (int r = 0; r < nc; ++r)
+                        acc -= a_coef(r, g[u], 0.0, 0.0, false) * s_res[slot[u]][r];
+                    xb = acc / q[u];
+                }
+                dual = smax(dual, abs_or_zero(xb - old[u]));
+                s.xbar[row[u]] = xb;
+            }
+            if (kZY) {
+                const double r = xv[u] - xb;
+                const double z = -(lam[u] + yv[u] + q[u] * r) / (q[u] + beta);
+                const double res = xv[u] - xb + z;
+                s.z[row[u]] = z;
+                s.y[row[u]] = yv[u] + q[u] * res;
+                pr = smax(pr, abs_or_zero(res));
+                zi = smax(zi, abs_or_zero(z));
+                zd = smax(zd, abs_or_zero(z - zv[u]));
+            }
         }
     }
     if (kZY) {

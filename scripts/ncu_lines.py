@@ -1,5 +1,7 @@
 """Join ncu per-SASS-instruction samples with nvdisasm line info.
-usage: ncu_lines.py <report.ncu-rep> <object.o> [kernel-substring]"""
+usage: ncu_lines.py <report.ncu-rep> <object.o> <kernel-substring> [callee-substring ...]
+The kernel's own function and any listed callees (noinline device functions)
+are concatenated in that order and aligned with ncu's SASS rows."""
 import csv, io, re, subprocess, sys, collections, os, tempfile
 rep, obj = sys.argv[1], sys.argv[2]
 tmp = tempfile.mkdtemp()
@@ -25,9 +27,10 @@ for r in rows:
 print("ncu rows", len(data), "funcs", {k[-40:]: len(v) for k, v in funcs.items()})
 # align: ncu lists kernel function then callees in address order; match by sass text sequence
 allins = []
-for k, v in funcs.items():
-    if "branch_persistent" in k or "drain_queue" in k:
-        allins += [(k, off, tag, txt) for off, tag, txt in v]
+for sub in sys.argv[3:]:
+    for k, v in funcs.items():
+        if sub in k:
+            allins += [(k, off, tag, txt) for off, tag, txt in v]
 agg = collections.Counter(); inst = collections.Counter(); tot = 0
 n = min(len(allins), len(data))
 mismatch = 0

@@ -102,8 +102,8 @@ enum AlAction : int { kAlContinue = 0, kAlDone = 1, kAlFailed = 2 };
 
 // A TRON solve ended with `status`: AL bookkeeping of kernels.cpp:246-271.
 // Either restarts TRON for the next AL round (kAlContinue) or ends the branch.
-template <int N, int S>
-__device__ __forceinline__ int al_after_solve(int status, Slot<S> slot, const BranchProb<N, S>& p,
+template <int N, int S, class BP>
+__device__ __forceinline__ int al_after_solve(int status, Slot<S> slot, const BP& p,
                                               TronState<N>& ts, int& al_it, double& prev_res) {
     for (;;) {
         if (status == kTronNumericalError) return kAlFailed;
@@ -161,8 +161,8 @@ __device__ __forceinline__ void finalize_branch(const DevNet& net, const DevStat
 }
 
 // Solve-level status of a TRON step that did not continue; updates iters.
-template <int N, int S, class Search>
-__device__ __forceinline__ int solve_status(int r, int iter_before, const BranchProb<N, S>& p,
+template <int N, int S, class Search, class BP>
+__device__ __forceinline__ int solve_status(int r, int iter_before, const BP& p,
                                             const TronState<N>& ts, const TronParams& tp,
                                             int& iters) {
     if (r == kStepConverged) { iters += iter_before; return kTronConverged; }
@@ -182,7 +182,11 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
     const int lane = threadIdx.x & 31;
     unsigned my_exec = 0;  // trust-region steps executed by this lane
     const Slot<kLaneBlock> slot{smem + threadIdx.x};
-    BranchProb<N, kLaneBlock> p{slot};
+#ifndef GA_LANE_HESS_SMEM
+#define GA_LANE_HESS_SMEM 0
+#endif
+    // GA_LANE_HESS_SMEM: Hessian in the slot (HessSmem); measured neutral at 70k
+    BranchProb<N, kLaneBlock, GA_LANE_HESS_SMEM != 0> p{slot};
     const TronParams tp = tron_params(cfg);
     const double kInf = __longlong_as_double(0x7ff0000000000000LL);
 
@@ -270,7 +274,13 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
     if (lane == 0 && warp_exec) atomicAdd(exec_dst, (unsigned long long)warp_exec);
 }
 
-__global__ void __launch_bounds__(kLaneBlock) lane_kernel(DevNet net, DevState st, BranchCfg cfg,
+#ifndef GA_LANE_MINB
+#define GA_LANE_MINB 1
+#endif
+#ifndef GA_TILE_MINB
+#define GA_TILE_MINB 1
+#endif
+__global__ void __launch_bounds__(kLaneBlock, GA_LANE_MINB) lane_kernel(DevNet net, DevState st, BranchCfg cfg,
                                                           Work w, DevScalars* sc) {
     extern __shared__ double smem[];
     unsigned long long it6 = 0, it4 = 0;
@@ -365,7 +375,7 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
     if (rank == 0 && my_exec) atomicAdd(exec_dst, my_exec);
 }
 
-__global__ void __launch_bounds__(kTileBlock) tile_kernel(DevNet net, DevState st, BranchCfg cfg,
+__global__ void __launch_bounds__(kTileBlock, GA_TILE_MINB) tile_kernel(DevNet net, DevState st, BranchCfg cfg,
                                                           Work w, DevScalars* sc) {
     __shared__ double smem[kFields * (kTileBlock / kTile)];
     unsigned long long it6 = 0, it4 = 0;
@@ -388,6 +398,8 @@ __global__ void __launch_bounds__(kTileBlock) tile_kernel(DevNet net, DevState s
 template <int N>
 struct QpProb {
     const double *H, *G, *L, *U;
+    template <int NN>
+    GA_FN HessRegs<NN> hess_store() const { return HessRegs<NN>{}; }
     GA_FN double lo(int i) const { return L[i]; }
     GA_FN double hi(int i) const { return U[i]; }
     GA_FN double value(const double* x) const {
@@ -491,7 +503,8 @@ void launch_branches(const DevNet& n, const DevState& s, const BranchCfg& cfg, D
     const Work w = work_of(n, s);
     cudaMemsetAsync(w.ctr, 0, kCounters * sizeof(int), st);
     static int lane_blocks = 0, tile_blocks = 0;
-    const size_t lane_smem = static_cast<size_t>(kFields) * kLaneBlock * sizeof(double);
+    const size_t lane_smem =
+        static_cast<size_t>(GA_LANE_HESS_SMEM ? kFieldsHess : kFields) * kLaneBlock * sizeof(double);
     if (lane_blocks == 0) {
         lane_blocks = persistent_blocks(lane_kernel, kLaneBlock, lane_smem);
         tile_blocks = persistent_blocks(tile_kernel, kTileBlock, 0);

@@ -21,6 +21,7 @@
 #include "device.hpp"
 #include "ga_math.h"
 #include "ga_sincos.h"
+#include "tron.cuh"
 
 namespace ga {
 namespace bp {
@@ -36,7 +37,9 @@ enum Field : int {
     F_RHO = 32,   // 8 penalties
     F_LTIJ = 40, F_LTJI = 41, F_RHOT = 42,
     F_VMIN_I = 43, F_VMAX_I = 44, F_VMIN_J = 45, F_VMAX_J = 46, F_R2 = 47,
-    kFields = 48
+    kFields = 48,
+    F_H = 48,            // lane phase: the TRON Hessian, 36 fields (HessSmem)
+    kFieldsHess = 84
 };
 
 // One branch's data: field f of slot s lives at smem[f * S + s].
@@ -157,11 +160,18 @@ struct YcView {
 };
 
 // The branch subproblem over a shared-memory slot (kernels.cpp:17-163).
-template <int N, int S>
+// kHessSmem: the TRON Hessian lives in the slot's F_H fields (lane phase).
+template <int N, int S, bool kHessSmem = false>
 struct BranchProb {
     static constexpr bool kLimited = N == 6;
     Slot<S> s;
     mutable double cc_, ss_;  // sincos at the last gradient point
+
+    template <int NN>
+    __device__ __forceinline__ auto hess_store() const {
+        if constexpr (kHessSmem) return HessSmem<S>{s.p + F_H * S};
+        else return HessRegs<NN>{};
+    }
 
     __device__ __forceinline__ double lo(int i) const {
         switch (i) {

@@ -74,8 +74,8 @@ template <int N>
 GA_FN double vnorm2(const double* a) { return sqrt(vdot<N>(a, a)); }
 
 // q(s) = g's + sum_i 0.5*s_i*(H s)_i  (tron.cpp:35-43)
-template <int N>
-GA_FN double model(const double* g, const double* h, const double* s) {
+template <int N, class HM>
+GA_FN double model(const double* g, const HM& h, const double* s) {
     double q = vdot<N>(g, s);
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -99,8 +99,8 @@ GA_FN double mdot(unsigned fm, const double* a, const double* b) {
 
 // Cholesky of the free principal submatrix (tron.cpp:53-67): reads the lower
 // triangle h[i][j], i > j, as the reference's hf does.
-template <int N>
-GA_FN bool mcholesky(unsigned fm, const double* h, double* L) {
+template <int N, class HM>
+GA_FN bool mcholesky(unsigned fm, const HM& h, double* L) {
 #pragma unroll
     for (int j = 0; j < N; ++j) {
         if (!(fm >> j & 1u)) continue;
@@ -158,8 +158,8 @@ GA_FN double boundary_tau(const double* s, const double* p, double delta) {
 }
 
 // Cauchy point (tron.cpp:101-137).
-template <int N>
-GA_FN void cauchy_point(const double* x, const double* g, const double* h,
+template <int N, class HM>
+GA_FN void cauchy_point(const double* x, const double* g, const HM& h,
                         const double* l, const double* u, double delta, double* s) {
     const double gnorm = vnorm2<N>(g);
     if (gnorm == 0.0) {
@@ -198,10 +198,91 @@ GA_FN void cauchy_point(const double* x, const double* g, const double* h,
     }
 }
 
+// Cauchy point with the backtracking trials evaluated B at a time.
+//
+// The reference's backtracking (tron.cpp:127-135) tries alpha0 * 2^-k for
+// k = 1..40 and stops at the first success; on the 70k-shaped grids it runs
+// ~21 trials per TRON iteration (alpha0 = 1 against Hessian eigenvalues
+// ~1e6), each a short dependent chain (clamp, norm, model).  The trials are
+// independent of each other, so one thread evaluates B consecutive ones side
+// by side (instruction-level parallelism) and takes the first success of the
+// batch — the trial the sequential loop stops at.  Round 0 speculatively
+// evaluates k = 0..B-1; if k = 0 succeeds the extrapolation branch runs
+// exactly as in cauchy_point.  Every trial uses the sequential loop's
+// expressions (alpha halved step by step), so the result is bit-identical.
+template <int N, int B, class HM>
+GA_FN void cauchy_point_batched(const double* x, const double* g, const HM& h,
+                                const double* l, const double* u, double delta, double* s) {
+    const double gnorm = vnorm2<N>(g);
+    if (gnorm == 0.0) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) s[i] = 0.0;
+        return;
+    }
+    auto step_at = [&](double alpha, double* out) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) out[i] = sclamp(x[i] - alpha * g[i], l[i], u[i]) - x[i];
+    };
+    auto ok = [&](const double* st) {
+        const bool in_region = vnorm2<N>(st) <= delta;
+        return in_region && model<N>(g, h, st) <= kTronMu0 * vdot<N>(g, st);
+    };
+    const double alpha0 = smin(1.0, delta / gnorm);
+    double a = alpha0;  // alpha of the next trial to form
+    for (int k0 = 0; k0 <= 40; k0 += B) {
+        double tr[B][N];
+        bool okb[B];
+        // branch-free over the batch so the B chains interleave
+        double nrm[B], mdl[B], gts[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            if (k0 + b > 0) a *= 0.5;  // trial k = k0 + b at alpha0 * 2^-k
+            step_at(a, tr[b]);
+        }
+#pragma unroll
+        for (int b = 0; b < B; ++b) nrm[b] = vdot<N>(tr[b], tr[b]);
+#pragma unroll
+        for (int b = 0; b < B; ++b) gts[b] = vdot<N>(g, tr[b]);
+#pragma unroll
+        for (int b = 0; b < B; ++b) mdl[b] = model<N>(g, h, tr[b]);
+#pragma unroll
+        for (int b = 0; b < B; ++b)
+            okb[b] = (k0 + b <= 40) & (sqrt(nrm[b]) <= delta) & (mdl[b] <= kTronMu0 * gts[b]);
+        if (k0 == 0 && okb[0]) {
+            // alpha0 accepted: extrapolate (tron.cpp:115-124)
+            double alpha = alpha0;
+#pragma unroll
+            for (int i = 0; i < N; ++i) s[i] = tr[0][i];
+            double trial[N];
+            for (int it = 0; it < 20; ++it) {
+                GA_STAT(1);
+                const double next = alpha * 2.0;
+                step_at(next, trial);
+                if (!ok(trial)) break;
+                alpha = next;
+#pragma unroll
+                for (int i = 0; i < N; ++i) s[i] = trial[i];
+            }
+            return;
+        }
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            const int k = k0 + b;
+            if (k == 0 || k > 40) continue;
+            GA_STAT(2);
+            if (okb[b] || k == 40) {  // first success, or the last trial's step
+#pragma unroll
+                for (int i = 0; i < N; ++i) s[i] = tr[b][i];
+                return;
+            }
+        }
+    }
+}
+
 // Preconditioned Steihaug CG on the free subspace at x + s
 // (tron.cpp:141-224).  d receives the full-space correction.
-template <int N>
-GA_FN void subspace_cg(const double* x, const double* g, const double* h,
+template <int N, class HM>
+GA_FN void subspace_cg(const double* x, const double* g, const HM& h,
                        const double* l, const double* u, double delta,
                        const TronParams& cfg, const double* s, double* d) {
 #pragma unroll
@@ -341,16 +422,38 @@ GA_FN bool tron_begin(const P& prob, TronState<N>& st) {
 
 enum TronStep : int { kStepContinue = 0, kStepConverged = 1, kStepError = 2, kStepExhausted = 3 };
 
+// Hessian storage of one solve: registers (HessRegs) or a strided column of
+// shared memory (HessSmem, the lane phase: frees 72 registers per thread for
+// occupancy / batched trials).  Both are read as h[i * N + j].
+template <int N>
+struct HessRegs {
+    double v[N * N];
+    GA_FN double operator[](int k) const { return v[k]; }
+    GA_FN void put(int k, double x) { v[k] = x; }
+};
+#if defined(__CUDACC__)
+template <int S>
+struct HessSmem {
+    double* p;  // element k at p[k * S]
+    __device__ __forceinline__ double operator[](int k) const { return p[k * S]; }
+    __device__ __forceinline__ void put(int k, double x) const { p[k * S] = x; }
+};
+#endif
+
 // Sequential search strategy (one thread per solve): the reference's loops.
+#ifndef GA_CAUCHY_B
+#define GA_CAUCHY_B 1
+#endif
 struct SerialSearch {
-    template <int N>
-    GA_FN void cauchy(const double* x, const double* g, const double* h, const double* l,
+    template <int N, class HM>
+    GA_FN void cauchy(const double* x, const double* g, const HM& h, const double* l,
                       const double* u, double delta, double* s) const {
-        cauchy_point<N>(x, g, h, l, u, delta, s);
+        if constexpr (GA_CAUCHY_B > 1) cauchy_point_batched<N, GA_CAUCHY_B>(x, g, h, l, u, delta, s);
+        else cauchy_point<N>(x, g, h, l, u, delta, s);
     }
     // Projected line search on s + beta d (tron.cpp:279-291); returns the step.
-    template <int N>
-    GA_FN void line_search(const double* x, const double* g, const double* h, const double* l,
+    template <int N, class HM>
+    GA_FN void line_search(const double* x, const double* g, const HM& h, const double* l,
                            const double* u, const double* s, const double* d, double qc,
                            double* stp) const {
         double beta = 1.0;
@@ -391,8 +494,8 @@ struct TileSearch {
         for (int i = 0; i < N; ++i) out[i] = __shfl_sync(mask, v[i], src, T);
     }
 
-    template <int N>
-    __device__ void cauchy(const double* x, const double* g, const double* h, const double* l,
+    template <int N, class HM>
+    __device__ void cauchy(const double* x, const double* g, const HM& h, const double* l,
                            const double* u, double delta, double* s) const {
         const double gnorm = vnorm2<N>(g);
         if (gnorm == 0.0) {
@@ -453,8 +556,8 @@ struct TileSearch {
         }
     }
 
-    template <int N>
-    __device__ void line_search(const double* x, const double* g, const double* h, const double* l,
+    template <int N, class HM>
+    __device__ void line_search(const double* x, const double* g, const HM& h, const double* l,
                                 const double* u, const double* s, const double* d, double qc,
                                 double* stp) const {
         double myst[N];
@@ -489,11 +592,16 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
     for (int i = 0; i < N; ++i)
         if (!sfinite(g[i])) return kStepError;
     if (proj_grad_norm<N>(st.x, g, l, u) <= cfg.gtol) return kStepConverged;
-    double h[N * N];
-    prob.hessian(st.x, h);
+    auto h = prob.template hess_store<N>();
+    {
+        double hr[N * N];
+        prob.hessian(st.x, hr);
 #pragma unroll
-    for (int i = 0; i < N * N; ++i)
-        if (!sfinite(h[i])) return kStepError;
+        for (int i = 0; i < N * N; ++i)
+            if (!sfinite(hr[i])) return kStepError;
+#pragma unroll
+        for (int i = 0; i < N * N; ++i) h.put(i, hr[i]);
+    }
     if (st.iter == 0 && st.delta == 0.0) st.delta = smax(vnorm2<N>(g), cfg.delta_floor);
 
     double s[N], d[N];

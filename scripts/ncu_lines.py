@@ -32,6 +32,8 @@ for sub in sys.argv[3:]:
         if sub in k:
             allins += [(k, off, tag, txt) for off, tag, txt in v]
 agg = collections.Counter(); inst = collections.Counter(); tot = 0
+REASONS = ["stall_no_inst", "stall_wait", "stall_long_sb", "stall_short_sb", "stall_branch_resolving", "stall_selected"]
+byr = collections.defaultdict(collections.Counter); rtot = collections.Counter()
 n = min(len(allins), len(data))
 mismatch = 0
 for i in range(n):
@@ -42,6 +44,11 @@ for i in range(n):
     if op_ncu.lstrip("@!P0123456789T") and op_ncu != op_dis and not op_dis.startswith("@"): mismatch += 1
     s = float(d["Warp Stall Sampling (All Samples)"] or 0)
     agg[tag] += s; inst[tag] += float(d["Instructions Executed"] or 0); tot += s
+    for r in REASONS:
+        v = float(d.get(r) or 0)
+        byr[tag][r] += v; rtot[r] += v
 print("mismatched opcodes", mismatch, "of", n)
+print("stall totals:", {r[6:]: int(v) for r, v in rtot.items()})
 for tag, s in agg.most_common(45):
-    print(f"{tag:24s} samples {s:8.0f} ({100*s/tot:5.1f}%)  inst {inst[tag]:12.0f}")
+    rs = " ".join(f"{r[6:]}={int(byr[tag][r])}" for r in REASONS if byr[tag][r] > 0.05 * s)
+    print(f"{tag:24s} samples {s:8.0f} ({100*s/tot:5.1f}%)  inst {inst[tag]:12.0f}  {rs}")

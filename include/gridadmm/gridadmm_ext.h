@@ -134,7 +134,9 @@ gridadmm_status gridadmm_session_timed_steps(gridadmm_session* s, int n,
 
 /* Total device time (ms) of the named kernel class since the session began,
  * measured with CUDA events on the session stream, and its launch count.
- * Classes: 0 gen, 1 branch, 2 bus, 3 zy (z+y+residual). */
+ * Classes: 0 gen, 1 branch (lane + tile phases), 2 bus (fused with z, y and
+ * the residual norms), 3 zy (0 since the fusion), 4 branch lane phase,
+ * 5 branch tile phase. */
 gridadmm_status gridadmm_session_kernel_time(const gridadmm_session* s,
                                              int kernel_class, double* ms,
                                              long long* launches);

@@ -36,7 +36,13 @@
 namespace ga {
 
 void tron_stats(unsigned long long out[8], bool reset) {
-#ifdef GA_TRON_STATS
+#ifdef GA_STEP_CLOCKS
+    cudaMemcpyFromSymbol(out, g_step_clocks, 8 * sizeof(unsigned long long));
+    if (reset) {
+        const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_step_clocks, z, sizeof z);
+    }
+#elif defined(GA_TRON_STATS)
     cudaMemcpyFromSymbol(out, g_tron_stats, 8 * sizeof(unsigned long long));
     if (reset) {
         const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -64,21 +70,27 @@ constexpr int kTileBlock = 128;  // tile phase: one slot per tile
 #define GA_TILE 8
 #endif
 constexpr int kTile = GA_TILE;   // lanes per branch in the tile phase
-constexpr int kCounters = 8;
+constexpr int kCounters = 12;
+constexpr int kSoloBlock = 32;  // solo phase: one warp per block, one branch per warp
 
-// Workspace: [overflow6 n_lim | overflow4 n_unl | counters]
-// counters: 0/1 lane-queue cursors (6/4), 2/3 overflow sizes, 4/5 tile cursors
+// Workspace: [overflow6 n_lim | overflow4 n_unl | solo6 n_lim | solo4 n_unl | counters]
+// counters: 0/1 lane-queue cursors (6/4), 2/3 overflow sizes, 4/5 tile cursors,
+//           6/7 solo sizes, 8/9 solo cursors
 struct Work {
     int* ovf6;
     int* ovf4;
+    int* solo6;
+    int* solo4;
     int* ctr;
 };
 
 Work work_of(const DevNet& n, const DevState& s) {
     Work w;
     w.ovf6 = s.branch_ws;
-    w.ovf4 = s.branch_ws + n.n_lim;
-    w.ctr = s.branch_ws + n.n_lim + n.n_unl;
+    w.ovf4 = w.ovf6 + n.n_lim;
+    w.solo6 = w.ovf4 + n.n_unl;
+    w.solo4 = w.solo6 + n.n_lim;
+    w.ctr = w.solo4 + n.n_unl;
     return w;
 }
 
@@ -153,8 +165,8 @@ __device__ __forceinline__ void finalize_branch(const DevNet& net, const DevStat
     xr[1] = make_double2(fl[2], fl[3]);
     xr[2] = make_double2(pt[0] * pt[0], pt[2]);
     xr[3] = make_double2(pt[1] * pt[1], pt[3]);
-#ifdef GA_TRON_STATS
-    (void)iters;  // stats build: br_cost = executed steps (+2^20 if the tile phase ran it)
+#if defined(GA_TRON_STATS) || defined(GA_BRANCH_STEPS)
+    (void)iters;  // stats builds: br_cost = executed steps (+2^20 if the tile phase ran it)
 #else
     st.br_cost[b] = iters;
 #endif
@@ -242,7 +254,7 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
                 const int status = solve_status<N, kLaneBlock, SerialSearch>(r, iter_before, p, ts,
                                                                             tp, iters);
                 const int act = al_after_solve<N>(status, slot, p, ts, al_it, prev_res);
-#ifdef GA_TRON_STATS
+#if defined(GA_TRON_STATS) || defined(GA_BRANCH_STEPS)
                 if (act != kAlContinue) st.br_cost[b] = steps + 1;
 #endif
                 if (act != kAlContinue) end_branch(act);
@@ -260,7 +272,7 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
                 st.lt_ij[b] = slot(F_LTIJ);
                 st.lt_ji[b] = slot(F_LTJI);
                 st.rho_t[b] = slot(F_RHOT);
-#ifdef GA_TRON_STATS
+#if defined(GA_TRON_STATS) || defined(GA_BRANCH_STEPS)
                 st.br_cost[b] = steps;
 #endif
                 ovf[atomicAdd(ovf_count, 1)] = b;
@@ -313,19 +325,22 @@ __global__ void __launch_bounds__(kLaneBlock, GA_LANE_MINB) lane_kernel(DevNet n
 }
 
 // ---- phase B: tiles of kTile lanes per overflow branch ---------------------
-template <int N>
+// Budget > 0: a branch still running after `budget` steps here is saved and
+// pushed to the solo queue (solo / solo_count), resumed by the solo phase.
+template <int N, int T>
 __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
                                         const BranchCfg& cfg, const int* ovf, const int* ovf_count,
                                         int* cursor, double* smem, unsigned long long* iters_out,
-                                        int* fail_out, unsigned long long* exec_dst) {
-    constexpr int S = kTileBlock / kTile;
+                                        int* fail_out, unsigned long long* exec_dst, int budget,
+                                        int* solo, int* solo_count) {
+    constexpr int S = kTileBlock / kTile;  // slots allocated (one per kTile lanes)
     unsigned long long my_exec = 0;
     const int lane = threadIdx.x & 31;
-    const int rank = lane & (kTile - 1);
-    const int tbase = lane & ~(kTile - 1);
-    const unsigned mask = ((1u << kTile) - 1u) << tbase;
-    const TileSearch<kTile> search{mask, tbase, rank};
-    const Slot<S> slot{smem + threadIdx.x / kTile};
+    const int rank = lane & (T - 1);
+    const int tbase = lane & ~(T - 1);
+    const unsigned mask = (T == 32 ? 0xffffffffu : ((1u << T) - 1u)) << tbase;
+    const TileSearch<T> search{mask, tbase, rank};
+    const Slot<S> slot{smem + threadIdx.x / T};
     BranchProb<N, S> p{slot};
     const TronParams tp = tron_params(cfg);
     const int count = *ovf_count;
@@ -334,7 +349,7 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
     for (;;) {
         int idx = 0;
         if (rank == 0) idx = atomicAdd(cursor, 1);
-        idx = __shfl_sync(mask, idx, 0, kTile);
+        idx = __shfl_sync(mask, idx, 0, T);
         if (idx >= count) break;
         const int b = ovf[idx];
         load_slot<S>(net, st, cfg, b, slot);
@@ -350,19 +365,44 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
         __syncwarp(mask);
         int act = kAlContinue;
         unsigned branch_exec = 0;
+        bool handed_off = false;
         while (act == kAlContinue) {
+            if (budget > 0 && branch_exec >= (unsigned)budget) {
+                // hand the solve to the solo phase with its exact state
+                __syncwarp(mask);
+                if (rank == 0) {
+#pragma unroll
+                    for (int k = 0; k < N; ++k) st.mig_x[k * net.nl + b] = ts.x[k];
+                    st.mig_f[b] = ts.f;
+                    st.mig_delta[b] = ts.delta;
+                    st.mig_iter[b] = ts.iter;
+                    st.mig_al[b] = al_it;
+                    st.mig_prev_res[b] = prev_res;
+                    st.mig_cost[b] = iters;
+                    st.lt_ij[b] = slot(F_LTIJ);
+                    st.lt_ji[b] = slot(F_LTJI);
+                    st.rho_t[b] = slot(F_RHOT);
+#if defined(GA_TRON_STATS) || defined(GA_BRANCH_STEPS)
+                    st.br_cost[b] += (int)branch_exec;
+#endif
+                    solo[atomicAdd(solo_count, 1)] = b;
+                }
+                handed_off = true;
+                break;
+            }
             const int iter_before = ts.iter;
             const int r = tron_step<N>(p, ts, tp, search);
             ++my_exec;
             ++branch_exec;
             if (r == kStepContinue) continue;
-            const int status = solve_status<N, S, TileSearch<kTile>>(r, iter_before, p, ts, tp, iters);
+            const int status = solve_status<N, S, TileSearch<T>>(r, iter_before, p, ts, tp, iters);
             act = al_after_solve<N>(status, slot, p, ts, al_it, prev_res);
         }
         __syncwarp(mask);
+        if (handed_off) continue;
         if (rank == 0) {
             finalize_branch<N>(net, st, slot, ts, b, act == kAlFailed, iters);
-#ifdef GA_TRON_STATS
+#if defined(GA_TRON_STATS) || defined(GA_BRANCH_STEPS)
             st.br_cost[b] += (int)branch_exec + (1 << 20);
 #endif
             my_iters += iters;
@@ -380,14 +420,61 @@ __global__ void __launch_bounds__(kTileBlock, GA_TILE_MINB) tile_kernel(DevNet n
     __shared__ double smem[kFields * (kTileBlock / kTile)];
     unsigned long long it6 = 0, it4 = 0;
     int fails = 0;
+    // Tail mode: when a queue holds no more branches than half the grid's
+    // warps, each branch gets a whole warp (T = 32: no other tile diverging in
+    // its warp, 32 search trials per round); otherwise 8-lane tiles.
+#ifndef GA_TILE_TAIL
+#define GA_TILE_TAIL 1
+#endif
+    const int half_warps = GA_TILE_TAIL ? gridDim.x * (kTileBlock / 32) / 2 : -1;
+    // 8-lane tiles hand branches that exceed cfg.tile_budget steps to the
+    // solo phase (one warp per branch, one block per SM).
+    auto run6 = [&] {
+        if (w.ctr[2] <= half_warps)
+            tile_phase<6, 32>(net, st, cfg, w.ovf6, &w.ctr[2], &w.ctr[4], smem, &it6, &fails, &sc->exec6,
+                              0, nullptr, nullptr);
+        else
+            tile_phase<6, kTile>(net, st, cfg, w.ovf6, &w.ctr[2], &w.ctr[4], smem, &it6, &fails,
+                                 &sc->exec6, cfg.tile_budget, w.solo6, &w.ctr[6]);
+    };
+    auto run4 = [&] {
+        if (w.ctr[3] <= half_warps)
+            tile_phase<4, 32>(net, st, cfg, w.ovf4, &w.ctr[3], &w.ctr[5], smem, &it4, &fails, &sc->exec4,
+                              0, nullptr, nullptr);
+        else
+            tile_phase<4, kTile>(net, st, cfg, w.ovf4, &w.ctr[3], &w.ctr[5], smem, &it4, &fails,
+                                 &sc->exec4, cfg.tile_budget, w.solo4, &w.ctr[7]);
+    };
     if ((sm_id() & 1u) == 0) {
-        tile_phase<6>(net, st, cfg, w.ovf6, &w.ctr[2], &w.ctr[4], smem, &it6, &fails, &sc->exec6);
-        tile_phase<4>(net, st, cfg, w.ovf4, &w.ctr[3], &w.ctr[5], smem, &it4, &fails, &sc->exec4);
+        run6();
+        run4();
     } else {
-        tile_phase<4>(net, st, cfg, w.ovf4, &w.ctr[3], &w.ctr[5], smem, &it4, &fails, &sc->exec4);
-        tile_phase<6>(net, st, cfg, w.ovf6, &w.ctr[2], &w.ctr[4], smem, &it6, &fails, &sc->exec6);
+        run4();
+        run6();
     }
     if ((threadIdx.x & (kTile - 1)) == 0) {
+        if (it6) atomicAdd(&sc->tron_iters6, it6);
+        if (it4) atomicAdd(&sc->tron_iters4, it4);
+        if (fails) atomicAdd(&sc->failures, (unsigned long long)fails);
+    }
+}
+
+// ---- phase C: solo warps for the few branches with very long solves -------
+// Late in a solve a handful of rate-limited branches run 10 AL rounds of up
+// to 200 TRON iterations (~1000 executed steps) while every other branch is
+// done in tens; the iteration then waits on their sequential chains.  Each
+// such branch gets a whole warp (32 search trials per round, no other tile
+// diverging in the warp) in a block of its own.
+__global__ void __launch_bounds__(kSoloBlock) solo_kernel(DevNet net, DevState st, BranchCfg cfg,
+                                                          Work w, DevScalars* sc) {
+    __shared__ double smem[kFields * (kTileBlock / kTile)];
+    unsigned long long it6 = 0, it4 = 0;
+    int fails = 0;
+    tile_phase<6, 32>(net, st, cfg, w.solo6, &w.ctr[6], &w.ctr[8], smem, &it6, &fails, &sc->exec6, 0,
+                      nullptr, nullptr);
+    tile_phase<4, 32>(net, st, cfg, w.solo4, &w.ctr[7], &w.ctr[9], smem, &it4, &fails, &sc->exec4, 0,
+                      nullptr, nullptr);
+    if (threadIdx.x == 0) {
         if (it6) atomicAdd(&sc->tron_iters6, it6);
         if (it4) atomicAdd(&sc->tron_iters4, it4);
         if (fails) atomicAdd(&sc->failures, (unsigned long long)fails);
@@ -494,26 +581,35 @@ int persistent_blocks(K kernel, int block, size_t smem) {
 }  // namespace
 
 size_t branch_workspace_ints(const DevNet& n) {
-    return static_cast<size_t>(n.n_lim) + n.n_unl + kCounters;
+    return 2 * (static_cast<size_t>(n.n_lim) + n.n_unl) + kCounters;
+}
+
+const int* branch_overflow_counts(const DevNet& n, const DevState& s) {
+    return work_of(n, s).ctr + 2;
 }
 
 void launch_branches(const DevNet& n, const DevState& s, const BranchCfg& cfg, DevScalars* sc,
-                     cudaStream_t st) {
+                     cudaStream_t st, cudaEvent_t mid) {
     if (n.nl <= 0) return;
     const Work w = work_of(n, s);
     cudaMemsetAsync(w.ctr, 0, kCounters * sizeof(int), st);
-    static int lane_blocks = 0, tile_blocks = 0;
+    static int lane_blocks = 0, tile_blocks = 0, solo_blocks = 0;
     const size_t lane_smem =
         static_cast<size_t>(GA_LANE_HESS_SMEM ? kFieldsHess : kFields) * kLaneBlock * sizeof(double);
     if (lane_blocks == 0) {
         lane_blocks = persistent_blocks(lane_kernel, kLaneBlock, lane_smem);
         tile_blocks = persistent_blocks(tile_kernel, kTileBlock, 0);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&solo_blocks, cudaDevAttrMultiProcessorCount, dev);
     }
     const int total = n.n_lim + n.n_unl;
     const int need = (total + kLaneBlock - 1) / kLaneBlock;
     lane_kernel<<<lane_blocks < need ? lane_blocks : need, kLaneBlock, lane_smem, st>>>(n, s, cfg,
                                                                                        w, sc);
+    if (mid) cudaEventRecord(mid, st);
     tile_kernel<<<tile_blocks, kTileBlock, 0, st>>>(n, s, cfg, w, sc);
+    if (cfg.tile_budget > 0) solo_kernel<<<solo_blocks, kSoloBlock, 0, st>>>(n, s, cfg, w, sc);
 }
 
 void launch_tron_qp(int count, int n, const double* h, const double* g, const double* l,
@@ -525,6 +621,8 @@ void launch_tron_qp(int count, int n, const double* h, const double* g, const do
     case NN:                                                                                     \
         if (tile == 8)                                                                           \
             tron_qp_kernel<NN, 8><<<blocks, 128, 0, st>>>(count, h, g, l, u, x, status, iterations); \
+        else if (tile == 32)                                                                     \
+            tron_qp_kernel<NN, 32><<<blocks, 128, 0, st>>>(count, h, g, l, u, x, status, iterations); \
         else                                                                                     \
             tron_qp_kernel<NN, 1><<<blocks, 128, 0, st>>>(count, h, g, l, u, x, status, iterations); \
         break;

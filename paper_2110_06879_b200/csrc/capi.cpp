@@ -108,6 +108,12 @@ const std::map<std::string, Field>& fields() {
                         [](gridadmm_config& c, double v) { c.solver.partitions = int(v); }}},
         {"devices", {true, 1.0, [](const gridadmm_config& c) { return double(c.solver.devices); },
                      [](gridadmm_config& c, double v) { c.solver.devices = int(v); }}},
+        // branch-phase scheduling (results do not depend on them): TRON steps a
+        // branch may take in the lane phase / the 8-lane tile phase (0 = no solo phase)
+        {"lane_budget", {true, 1.0, [](const gridadmm_config& c) { return double(c.solver.tron.lane_budget); },
+                         [](gridadmm_config& c, double v) { c.solver.tron.lane_budget = int(v); }}},
+        {"tile_budget", {true, 0.0, [](const gridadmm_config& c) { return double(c.solver.tron.tile_budget); },
+                         [](gridadmm_config& c, double v) { c.solver.tron.tile_budget = int(v); }}},
     };
     return f;
 }
@@ -253,7 +259,9 @@ gridadmm_status gridadmm_solve(const gridadmm_network* net, const gridadmm_confi
                                gridadmm_report** out) {
     if (!net || !cfg || !out) return fail(GRIDADMM_ERR_INVALID_ARG, "null argument to solve");
     try {
+        ga::trace_phase("gridadmm_solve entry");
         std::unique_ptr<ga::Engine> eng = ga::make_engine(net->net, cfg->solver);
+        ga::trace_phase("engine ready");
         auto* rep = new gridadmm_report{ga::solve(*eng, cfg->solver, false), net->net};
         *out = rep;
         const gridadmm_status s = status_of(rep->report.status);
@@ -497,7 +505,7 @@ gridadmm_status gridadmm_session_timed_steps(gridadmm_session* s, int n, size_t 
 
 gridadmm_status gridadmm_session_kernel_time(const gridadmm_session* s, int cls, double* ms,
                                              long long* launches) {
-    if (!s || cls < 0 || cls > 3) return fail(GRIDADMM_ERR_INVALID_ARG, "bad argument to kernel_time");
+    if (!s || cls < 0 || cls > 5) return fail(GRIDADMM_ERR_INVALID_ARG, "bad argument to kernel_time");
     if (!s->s) return fail(GRIDADMM_ERR_INVALID_ARG, "kernel_time needs a single-part session");
     const ga::KernelClock c = s->s->kernel_clock(cls);
     if (ms) *ms = c.ms;
@@ -550,7 +558,7 @@ int gridadmm_device_count(void) {
 gridadmm_status gridadmm_probe_tron_qp(int count, int n, const double* h, const double* g,
                                        const double* l, const double* u, double* x, int* status,
                                        int* iterations, int tile) {
-    if (count < 0 || n < 1 || n > 6 || (tile != 1 && tile != 8))
+    if (count < 0 || n < 1 || n > 6 || (tile != 1 && tile != 8 && tile != 32))
         return fail(GRIDADMM_ERR_INVALID_ARG, "bad qp batch");
     return guarded([&]() -> gridadmm_status {
         const size_t nn = static_cast<size_t>(count) * n;

@@ -102,12 +102,16 @@ struct BranchCfg {
     double delta_floor = 1e-3;
     double limit_tighten = 0.99;
     int lane_budget = 4;  // TRON iterations a branch may take in the lane phase (swept: 4 best)
+    int tile_budget = 48; // steps in the 8-lane tile phase before the solo phase takes over (0 = off)
 };
 
 // ---- launchers (kernels.cu / branch.cu) ----------------------------------
 void launch_generators(const DevNet& n, const DevState& s, cudaStream_t st);
+// `mid` (optional) is recorded between the lane-phase and tile-phase kernels.
 void launch_branches(const DevNet& n, const DevState& s, const BranchCfg& cfg,
-                     DevScalars* sc, cudaStream_t st);
+                     DevScalars* sc, cudaStream_t st, cudaEvent_t mid = nullptr);
+// Overflow queue sizes (6-var, 4-var) of the last branch sweep (device ints).
+const int* branch_overflow_counts(const DevNet& n, const DevState& s);
 void launch_buses(const DevNet& n, const DevState& s, DevScalars* sc, cudaStream_t st);
 // Bus QP fused with z, y and all four residual norms (the iteration path).
 void launch_bus_zy(const DevNet& n, const DevState& s, double beta, DevScalars* sc,

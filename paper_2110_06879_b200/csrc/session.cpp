@@ -2,6 +2,7 @@
 // sequence of one inner iteration (proj/src/driver.cpp:155-186).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "ga_math.h"
@@ -31,11 +32,18 @@ double SolverConfig::effective_inner_tol(int m) const {
 Session::Session(const Network& net, const SolverConfig& cfg, const PartPlan* plan)
     : net_(net), cfg_(cfg) {
     if (plan) plan_ = *plan;
+    trace_phase("session: network copy");
     check(cudaSetDevice(cfg.device), "cudaSetDevice");
     check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
     for (auto& e : ev_) check(cudaEventCreate(&e), "cudaEventCreate");
+    if (const char* pf = std::getenv("GRIDADMM_PROFILE")) {
+        prof_ = std::fopen(pf, "a");
+        if (prof_) std::fprintf(prof_, "iter,gen_ms,lane_ms,tile_ms,bus_zy_ms,ovf6,ovf4,beta\n");
+    }
+    trace_phase("session: stream/events");
     try {
         upload_network();
+        trace_phase("session: upload network");
         check(cudaMalloc(&sc_, sizeof(DevScalars)), "cudaMalloc scalars");
         check(cudaMemset(sc_, 0, sizeof(DevScalars)), "cudaMemset scalars");
         check(cudaMallocHost(&sc_host_, sizeof(DevScalars)), "cudaMallocHost");
@@ -63,6 +71,8 @@ void Session::free_all() {
     sc_host_ = nullptr;
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
+    if (prof_) std::fclose(prof_);
+    prof_ = nullptr;
     if (stream_) cudaStreamDestroy(stream_);
     stream_ = nullptr;
 }
@@ -325,6 +335,11 @@ BranchCfg branch_cfg(const SolverConfig& c) {
         return e ? std::atoi(e) : -1;
     }();
     if (budget >= 1) b.lane_budget = budget;
+    static const int tile_budget = [] {
+        const char* e = std::getenv("GRIDADMM_TILE_BUDGET");
+        return e ? std::atoi(e) : -1;
+    }();
+    if (tile_budget >= 0) b.tile_budget = tile_budget;
     return b;
 }
 
@@ -389,25 +404,40 @@ int Session::iterate_ev(double out[4], PhaseTimes* times, cudaEvent_t end_event)
     cudaEventRecord(ev_[0], stream_);
     launch_generators(dn_, ds_, stream_);
     cudaEventRecord(ev_[1], stream_);
-    launch_branches(dn_, ds_, branch_cfg(cfg_), sc_, stream_);
+    launch_branches(dn_, ds_, branch_cfg(cfg_), sc_, stream_, ev_[5]);
     cudaEventRecord(ev_[2], stream_);
     launch_bus_zy(dn_, ds_, beta_, sc_, stream_);
     cudaEventRecord(ev_[3], stream_);
     cudaEventRecord(ev_[4], stream_);
     check(cudaGetLastError(), "iteration launch");
     check(cudaMemcpyAsync(sc_host_, sc_, sizeof(DevScalars), cudaMemcpyDeviceToHost, stream_), "D2H");
+    int ovf[2] = {0, 0};
+    if (prof_ && dn_.nl)
+        check(cudaMemcpyAsync(ovf, branch_overflow_counts(dn_, ds_), sizeof ovf,
+                              cudaMemcpyDeviceToHost, stream_), "D2H");
     if (end_event) cudaEventRecord(end_event, stream_);
     check(cudaStreamSynchronize(stream_), "iteration sync");
-    float ms[4] = {0, 0, 0, 0};
+    float ms[4] = {0, 0, 0, 0}, lane = 0.0f, tile = 0.0f;
     for (int k = 0; k < 4; ++k) {
         cudaEventElapsedTime(&ms[k], ev_[k], ev_[k + 1]);
         clocks_[k].ms += ms[k];
         clocks_[k].launches += 1;
     }
+    if (dn_.nl) {
+        cudaEventElapsedTime(&lane, ev_[1], ev_[5]);
+        cudaEventElapsedTime(&tile, ev_[5], ev_[2]);
+    }
+    clocks_[4].ms += lane;
+    clocks_[4].launches += 1;
+    clocks_[5].ms += tile;
+    clocks_[5].launches += 1;
+    if (prof_)
+        std::fprintf(prof_, "%ld,%.4f,%.4f,%.4f,%.4f,%d,%d,%.6g\n", ++prof_it_, ms[0], lane, tile,
+                     ms[2], ovf[0], ovf[1], beta_);
     if (times) {
         times->x_s += (ms[0] + ms[1]) * 1e-3;
         times->xbar_s += ms[2] * 1e-3;
-        times->z_s += ms[3] * 1e-3;  // z and y are one fused kernel
+        times->z_s += ms[3] * 1e-3;  // z and y are fused into the bus kernel
     }
     const DevScalars& h = *sc_host_;
     if (h.singular_bus != INT32_MAX) {

@@ -22,6 +22,23 @@ namespace {
 
 using Clock = std::chrono::steady_clock;
 
+}  // namespace
+
+void trace_phase(const char* what) {
+    static const bool on = [] {
+        const char* e = std::getenv("GRIDADMM_TRACE");
+        return e && *e == '1';
+    }();
+    if (!on) return;
+    static Clock::time_point last = Clock::now();
+    const auto now = Clock::now();
+    std::fprintf(stderr, "[gridadmm] %-28s +%9.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+}
+
+namespace {
+
 double seconds_since(Clock::time_point t0) {
     return std::chrono::duration<double>(Clock::now() - t0).count();
 }
@@ -115,10 +132,13 @@ QualityMetrics evaluate_solution(const Network& net, const Solution& sol) {
 namespace {
 
 void finish_report(Engine& s, SolveReport& rep) {
+    trace_phase("iteration loop");
     std::vector<double> gen_rows, w, th;
     s.download_solution_inputs(gen_rows, w, th);
+    trace_phase("solution download");
     rep.solution = extract_solution(s.network(), gen_rows, w, th);
     rep.quality = evaluate_solution(s.network(), rep.solution);
+    trace_phase("extract + evaluate");
 }
 
 }  // namespace
@@ -126,11 +146,14 @@ void finish_report(Engine& s, SolveReport& rep) {
 // driver.cpp:140-246.  warm == false -> cold start on the device state.
 SolveReport solve(Engine& s, const SolverConfig& cfg, bool warm) {
     const auto t0 = Clock::now();
+    trace_phase("solve entry");
     if (!warm) s.cold_start();
+    trace_phase("cold start + upload");
     SolveReport report;
     const double inner_tol = cfg.effective_inner_tol(s.m());
     double prev_z_inf = -1.0;
     const double rho_max = s.rho_max();
+    trace_phase("rho_max");
     double last_z_inf = 0.0;
 
     for (int outer = 1; outer <= cfg.max_outer; ++outer) {

@@ -14,6 +14,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <cstdio>
 #include <vector>
 
 #include "device.hpp"
@@ -221,8 +222,10 @@ private:
     size_t flush_size_ = 0;
     double beta_ = 0.0;
     cudaStream_t stream_ = nullptr;
-    cudaEvent_t ev_[5] = {};
-    KernelClock clocks_[4];
+    cudaEvent_t ev_[6] = {};
+    KernelClock clocks_[6];  // gen, branch, bus(+z/y), zy (fused: 0), lane phase, tile phase
+    std::FILE* prof_ = nullptr;  // GRIDADMM_PROFILE=<csv>: per-iteration kernel times
+    long prof_it_ = 0;
     std::vector<void*> allocs_;
     PartPlan plan_;
     std::vector<int*> d_send_, d_recv_;
@@ -276,6 +279,10 @@ void write_solution_json(const std::string& path, const Network& net, const Solv
 void write_convergence_csv(const std::string& path, const std::vector<IterationRecord>& s);
 void write_periods_csv(const std::string& path, const std::vector<PeriodReport>& p,
                        const std::vector<double>& refs);
+
+// GRIDADMM_TRACE=1: host-side phase timings of a solve on stderr
+// (engine setup, cold start, iteration loop, solution extraction).
+void trace_phase(const char* what);
 
 }  // namespace ga
 

@@ -36,6 +36,27 @@ __device__ unsigned long long g_tron_stats[8];  // tron.cuh is included by one T
 #define GA_STAT(k) ((void)0)
 #endif
 
+// Optional section clocks (debug builds with -DGA_STEP_CLOCKS): cycles of
+// the step sections of solves run by a search strategy that opts in
+// (Search::kClocked), summed into g_step_clocks[section].
+#if defined(GA_STEP_CLOCKS)
+__device__ unsigned long long g_step_clocks[8];
+#endif
+#if defined(GA_STEP_CLOCKS) && defined(__CUDA_ARCH__)
+#define GA_CLK_DECL long long ga_clk_t0 = clock64();
+#define GA_CLK(k)                                                                     \
+    do {                                                                              \
+        if (Search::kClocked) {                                                       \
+            const long long ga_clk_t1 = clock64();                                    \
+            if ((threadIdx.x & 31) == 0) atomicAdd(&g_step_clocks[k], ga_clk_t1 - ga_clk_t0); \
+            ga_clk_t0 = ga_clk_t1;                                                    \
+        }                                                                             \
+    } while (0)
+#else
+#define GA_CLK_DECL
+#define GA_CLK(k) ((void)0)
+#endif
+
 struct TronParams {           // proj/src/tron.hpp:24-30
     double gtol = 1e-6;
     int max_iterations = 200;
@@ -445,6 +466,7 @@ struct HessSmem {
 #define GA_CAUCHY_B 1
 #endif
 struct SerialSearch {
+    static constexpr bool kClocked = false;
     template <int N, class HM>
     GA_FN void cauchy(const double* x, const double* g, const HM& h, const double* l,
                       const double* u, double delta, double* s) const {
@@ -481,6 +503,7 @@ struct SerialSearch {
 // two is exact), so the selected step is bit-identical.
 template <int T>
 struct TileSearch {
+    static constexpr bool kClocked = T == 32;
     unsigned mask;  // warp lanes of this tile
     int base;       // first warp lane of the tile
     int rank;       // lane within the tile
@@ -586,12 +609,14 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
     double l[N], u[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) { l[i] = prob.lo(i); u[i] = prob.hi(i); }
+    GA_CLK_DECL
     double g[N];
     prob.gradient(st.x, g);
 #pragma unroll
     for (int i = 0; i < N; ++i)
         if (!sfinite(g[i])) return kStepError;
     if (proj_grad_norm<N>(st.x, g, l, u) <= cfg.gtol) return kStepConverged;
+    GA_CLK(0);
     auto h = prob.template hess_store<N>();
     {
         double hr[N * N];
@@ -605,8 +630,11 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
     if (st.iter == 0 && st.delta == 0.0) st.delta = smax(vnorm2<N>(g), cfg.delta_floor);
 
     double s[N], d[N];
+    GA_CLK(1);
     search.template cauchy<N>(st.x, g, h, l, u, st.delta, s);
+    GA_CLK(2);
     subspace_cg<N>(st.x, g, h, l, u, st.delta, cfg, s, d);
+    GA_CLK(3);
 
     const double qc = model<N>(g, h, s);
     double stp[N];
@@ -615,7 +643,9 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
     double xt[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) xt[i] = sclamp(st.x[i] + stp[i], l[i], u[i]);
+    GA_CLK(4);
     const double ft = prob.value(xt);
+    GA_CLK(5);
     if (!sfinite(ft)) return kStepError;
     const double ared = st.f - ft;
     const double pred = -q;
@@ -644,6 +674,10 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
         GA_STAT(5);
         st.iter = cfg.max_iterations;
     }
+    GA_CLK(6);
+#if defined(GA_STEP_CLOCKS) && defined(__CUDA_ARCH__)
+    if (Search::kClocked && (threadIdx.x & 31) == 0) atomicAdd(&g_step_clocks[7], 1ull);
+#endif
     if (st.delta < 1e-14 || st.iter >= cfg.max_iterations) return kStepExhausted;
     return kStepContinue;
 }

@@ -34,7 +34,17 @@ for o in range(outers):
           f"kernels/5 {[round((k1[i][0] - k0[i][0]) / 5, 3) for i in range(4)]} "
           f"tron(ref) {[c1[i] - c0[i] for i in (0, 1)]} exec {[c1[i] - c0[i] for i in (2, 3)]}",
           flush=True)
+    lib_name = os.environ.get("GRIDADMM_LIB", "")
+    stats_build = "stats" in lib_name or "steps" in lib_name
     for name, sel in (("lim", limited), ("unl", ~limited)):
         cc = c[sel]
-        print(f"   {name}: mean {cc.mean():.1f} p50/90/99/max {np.percentile(cc, [50, 90, 99, 100])} "
-              f"n>=200 {(cc >= 200).sum()} n>=1000 {(cc >= 1000).sum()}", flush=True)
+        if stats_build:  # br_cost = executed steps (+2^20 when the tile phase ran it)
+            ovf = cc >= (1 << 20)
+            stp = cc & ((1 << 20) - 1)
+            t = stp[ovf]
+            print(f"   {name}: lane-only {(~ovf).sum()} steps {stp[~ovf].sum()} | overflow {ovf.sum()} "
+                  f"steps {t.sum()} p50/90/99/max {np.percentile(t, [50, 90, 99, 100]) if t.size else []}",
+                  flush=True)
+        else:
+            print(f"   {name}: mean {cc.mean():.1f} p50/90/99/max {np.percentile(cc, [50, 90, 99, 100])} "
+                  f"n>=200 {(cc >= 200).sum()} n>=1000 {(cc >= 1000).sum()}", flush=True)

@@ -62,12 +62,12 @@ def test_device_sincos_matches_host_shim(gridadmm, oracle_mod):
     assert_bits_equal(cd, ch, "cos")
 
 
-@pytest.mark.parametrize("tile", [1, 8])
+@pytest.mark.parametrize("tile", [1, 8, 32])
 @pytest.mark.parametrize("n", [4, 6, 2])
 def test_tron_core_matches_reference(gridadmm, oracle_mod, n, tile):
     """Batched device TRON vs reference solve_one on random box QPs (convex and
     indefinite), acceptance.cpp:458-520 style, in both the one-lane (serial
-    search) and the 8-lane tile (speculative search) formulations."""
+    search), the 8-lane tile and the whole-warp (speculative search) formulations."""
     rng = np.random.default_rng(100 + n)
     count = 4000
     A = rng.normal(size=(count, n, n))
@@ -166,3 +166,27 @@ def test_full_solve_case9_through_c_abi(gridadmm, oracle_mod, tmp_path):
     rows = np.loadtxt(conv, delimiter=",", skiprows=1)
     assert rows.shape[0] == series.shape[0]
     assert_bits_equal(rows[:, 2:5], series[:, 2:5], "convergence.csv")
+
+
+@pytest.mark.parametrize("name", ["case30", "case118", "case9"])
+@pytest.mark.parametrize("lane_budget,tile_budget", [(1, 1), (1, 0), (2, 3)])
+def test_branch_schedule_invariance(gridadmm, oracle_mod, name, lane_budget, tile_budget):
+    """The branch phase's schedule (lane phase -> 8-lane tiles -> solo warps,
+    with exact state hand-offs) must not change a bit: tiny budgets push
+    nearly every branch through every phase; series and final state must
+    still equal the reference's."""
+    iters = 40
+    net = gridadmm.Network(case_path(name))
+    cfg, d = make_cfg(gridadmm, name)
+    cfg["lane_budget"] = lane_budget
+    cfg["tile_budget"] = tile_budget
+    sess = gridadmm.Session(net, cfg)
+    rec, _ = sess.iterate(iters)
+    ref = oracle_mod.RefNet(case_path(name))
+    series, info, fin = ref.solve(**dict(d, max_outer=1, max_inner=iters))
+    assert len(rec) == len(series)
+    assert_bits_equal(rec[:, 0:3], series[:, 2:5], f"{name} residuals")
+    z_last = float(rec[-1, 2])
+    if not z_last <= d["eps"]:
+        sess.phase("outer", z_last, -1.0)
+    assert_state_equal(sess.get_state(), fin, f"{name} final")

@@ -75,7 +75,7 @@ constexpr int kSoloBlock = 32;  // solo phase: one warp per block, one branch pe
 
 // Workspace: [overflow6 n_lim | overflow4 n_unl | solo6 n_lim | solo4 n_unl | counters]
 // counters: 0/1 lane-queue cursors (6/4), 2/3 overflow sizes, 4/5 tile cursors,
-//           6/7 solo sizes, 8/9 solo cursors
+//           6/7 solo sizes, 8/9 solo cursors, 10/11 lane-phase branches done or handed on
 struct Work {
     int* ovf6;
     int* ovf4;
@@ -189,7 +189,7 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
                                         const BranchCfg& cfg, const int* list, int count,
                                         int* cursor, int* ovf, int* ovf_count, double* smem,
                                         unsigned long long* iters_out, int* fail_out,
-                                        unsigned long long* exec_dst) {
+                                        unsigned long long* exec_dst, int* done_ctr) {
     constexpr unsigned kFull = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     unsigned my_exec = 0;  // trust-region steps executed by this lane
@@ -215,6 +215,7 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
         finalize_branch<N>(net, st, slot, ts, b, failed, iters);
         my_iters += iters;
         my_fail += failed ? 1 : 0;
+        atomicAdd(done_ctr, 1);
         b = -1;
     };
     for (;;) {
@@ -246,6 +247,16 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
             }
         }
         if (__all_sync(kFull, b < 0 && exhausted)) break;
+        // Throughput mode while more branches are still active than the tile
+        // phase has tiles for: a branch may take up to lane_cap steps here
+        // (32 branches per warp beat 4 per warp when there is enough work).
+        // Once the active set fits the tiles, branches past lane_budget move
+        // to the tile phase, whose parallel searches have the shorter
+        // per-step latency.
+        int active = 0;
+        if (lane == 0) active = count - *reinterpret_cast<volatile int*>(done_ctr);
+        active = __shfl_sync(kFull, active, 0);
+        const int budget = active <= cfg.tile_slots ? cfg.lane_budget : cfg.lane_cap;
         if (b >= 0) {
             const int iter_before = ts.iter;
             const int r = tron_step<N>(p, ts, tp);
@@ -259,7 +270,7 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
 #endif
                 if (act != kAlContinue) end_branch(act);
             }
-            if (b >= 0 && ++steps >= cfg.lane_budget) {
+            if (b >= 0 && ++steps >= budget) {
                 // hand the solve to the tile phase with its exact state
 #pragma unroll
                 for (int k = 0; k < N; ++k) st.mig_x[k * net.nl + b] = ts.x[k];
@@ -276,6 +287,7 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
                 st.br_cost[b] = steps;
 #endif
                 ovf[atomicAdd(ovf_count, 1)] = b;
+                atomicAdd(done_ctr, 1);
                 b = -1;
             }
         }
@@ -301,14 +313,14 @@ __global__ void __launch_bounds__(kLaneBlock, GA_LANE_MINB) lane_kernel(DevNet n
     // so each SM's warps share one code path (instruction-cache locality).
     if ((sm_id() & 1u) == 0) {
         lane_phase<6>(net, st, cfg, net.lim_list, net.n_lim, &w.ctr[0], w.ovf6, &w.ctr[2], smem,
-                      &it6, &fails, &sc->exec6);
+                      &it6, &fails, &sc->exec6, &w.ctr[10]);
         lane_phase<4>(net, st, cfg, net.unl_list, net.n_unl, &w.ctr[1], w.ovf4, &w.ctr[3], smem,
-                      &it4, &fails, &sc->exec4);
+                      &it4, &fails, &sc->exec4, &w.ctr[11]);
     } else {
         lane_phase<4>(net, st, cfg, net.unl_list, net.n_unl, &w.ctr[1], w.ovf4, &w.ctr[3], smem,
-                      &it4, &fails, &sc->exec4);
+                      &it4, &fails, &sc->exec4, &w.ctr[11]);
         lane_phase<6>(net, st, cfg, net.lim_list, net.n_lim, &w.ctr[0], w.ovf6, &w.ctr[2], smem,
-                      &it6, &fails, &sc->exec6);
+                      &it6, &fails, &sc->exec6, &w.ctr[10]);
     }
     const unsigned full = 0xffffffffu;
 #pragma unroll
@@ -426,7 +438,7 @@ __global__ void __launch_bounds__(kTileBlock, GA_TILE_MINB) tile_kernel(DevNet n
 #ifndef GA_TILE_TAIL
 #define GA_TILE_TAIL 1
 #endif
-    const int half_warps = GA_TILE_TAIL ? gridDim.x * (kTileBlock / 32) / 2 : -1;
+    const int half_warps = GA_TILE_TAIL ? (int)(gridDim.x * (kTileBlock / 32) / 2) : -1;
     // 8-lane tiles hand branches that exceed cfg.tile_budget steps to the
     // solo phase (one warp per branch, one block per SM).
     auto run6 = [&] {
@@ -562,6 +574,67 @@ __global__ void tron_qp_kernel(int count, const double* H, const double* G, cons
     }
 }
 
+// ---- cold start on the device (driver.cpp:26-63, decomp.cpp:37-57) -------
+// Same expressions as Session's host restatement; items: rows (z, y, lambda,
+// rho), branches (8 x / xbar rows, point, multipliers), generators (2 rows),
+// buses (w, theta).  Every x / xbar row is written by exactly one item.
+__global__ void cold_start_kernel(DevNet n, DevState s, double rho_pq, double rho_va,
+                                  double limit_tighten) {
+    const long long total = (long long)n.m + n.nl + n.ng + n.nb;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        if (t < n.m) {
+            const int k = (int)t;
+            const bool pq = k < 2 * n.ng || (k - 2 * n.ng) % 8 < 4;
+            s.z[k] = 0.0;
+            s.y[k] = 0.0;
+            s.lambda[k] = 0.0;
+            s.rho[k] = pq ? rho_pq : rho_va;
+        } else if (t < (long long)n.m + n.nl) {
+            const int b = (int)(t - n.m);
+            const int from = n.br_from[b], to = n.br_to[b];
+            const double vi = 0.5 * (n.b_vmin[from] + n.b_vmax[from]);
+            const double vj = 0.5 * (n.b_vmin[to] + n.b_vmax[to]);
+            const YArr yc{n.br_y, n.nl, b};
+            double f[4];
+            bp::branch_flows(yc, vi, vj, 0.0, 0.0, f);
+            const double vals[8] = {f[0], f[1], f[2], f[3], vi * vi, 0.0, vj * vj, 0.0};
+            const int base = 2 * n.ng + 8 * b;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                s.x[base + k] = vals[k];
+                s.xbar[base + k] = vals[k];
+            }
+            double sij = 0.0, sji = 0.0;
+            const double rate = n.br_rate[b];
+            if (rate > 0.0) {
+                const double rt = limit_tighten * rate;
+                sij = sclamp(-(f[0] * f[0] + f[1] * f[1]), -rt * rt, 0.0);
+                sji = sclamp(-(f[2] * f[2] + f[3] * f[3]), -rt * rt, 0.0);
+            }
+            const double pt[6] = {vi, vj, 0.0, 0.0, sij, sji};
+#pragma unroll
+            for (int k = 0; k < 6; ++k) s.bp[k * n.nl + b] = pt[k];
+            s.lt_ij[b] = 0.0;
+            s.lt_ji[b] = 0.0;
+            s.rho_t[b] = rho_pq;
+        } else if (t < (long long)n.m + n.nl + n.ng) {
+            const int g = (int)(t - n.m - n.nl);
+            const double p = 0.5 * (n.g_pmin[g] + n.g_pmax[g]);
+            const double q = 0.5 * (n.g_qmin[g] + n.g_qmax[g]);
+            s.x[2 * g] = p;
+            s.xbar[2 * g] = p;
+            s.x[2 * g + 1] = q;
+            s.xbar[2 * g + 1] = q;
+        } else {
+            const int i = (int)(t - n.m - n.nl - n.ng);
+            const double v = 0.5 * (n.b_vmin[i] + n.b_vmax[i]);
+            s.bus_w[i] = v * v;
+            s.bus_theta[i] = 0.0;
+        }
+    }
+}
+
 __global__ void sincos_probe_kernel(const double* x, double* s, double* c, int n) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k < n) ga_sincos(x[k], &s[k], &c[k]);
@@ -605,7 +678,9 @@ void launch_branches(const DevNet& n, const DevState& s, const BranchCfg& cfg, D
     }
     const int total = n.n_lim + n.n_unl;
     const int need = (total + kLaneBlock - 1) / kLaneBlock;
-    lane_kernel<<<lane_blocks < need ? lane_blocks : need, kLaneBlock, lane_smem, st>>>(n, s, cfg,
+    BranchCfg lc = cfg;
+    lc.tile_slots = tile_blocks * (kTileBlock / kTile) / 2;  // per queue (two queues share)
+    lane_kernel<<<lane_blocks < need ? lane_blocks : need, kLaneBlock, lane_smem, st>>>(n, s, lc,
                                                                                        w, sc);
     if (mid) cudaEventRecord(mid, st);
     tile_kernel<<<tile_blocks, kTileBlock, 0, st>>>(n, s, cfg, w, sc);
@@ -631,6 +706,15 @@ void launch_tron_qp(int count, int n, const double* h, const double* g, const do
         default: break;
     }
 #undef GA_QP
+}
+
+void launch_cold_start(const DevNet& n, const DevState& s, double rho_pq, double rho_va,
+                       double limit_tighten, cudaStream_t st) {
+    const long long total = (long long)n.m + n.nl + n.ng + n.nb;
+    if (total <= 0) return;
+    long long blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    cold_start_kernel<<<(int)blocks, 256, 0, st>>>(n, s, rho_pq, rho_va, limit_tighten);
 }
 
 void launch_sincos_probe(const double* x, double* s, double* c, int n, cudaStream_t st) {

@@ -322,6 +322,13 @@ struct BranchProb {
     }
 };
 
+// Admittance view over the global [8][nl] array (cold start).
+struct YArr {
+    const double* y;
+    int nl, b;
+    __device__ __forceinline__ double operator()(int k) const { return y[k * nl + b]; }
+};
+
 // branch_flows (netdata.cpp:33-45)
 template <class Y>
 GA_FN void branch_flows(const Y& yc, double vi, double vj, double thi, double thj, double* out) {

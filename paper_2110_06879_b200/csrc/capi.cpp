@@ -112,6 +112,8 @@ const std::map<std::string, Field>& fields() {
         // branch may take in the lane phase / the 8-lane tile phase (0 = no solo phase)
         {"lane_budget", {true, 1.0, [](const gridadmm_config& c) { return double(c.solver.tron.lane_budget); },
                          [](gridadmm_config& c, double v) { c.solver.tron.lane_budget = int(v); }}},
+        {"lane_cap", {true, 1.0, [](const gridadmm_config& c) { return double(c.solver.tron.lane_cap); },
+                      [](gridadmm_config& c, double v) { c.solver.tron.lane_cap = int(v); }}},
         {"tile_budget", {true, 0.0, [](const gridadmm_config& c) { return double(c.solver.tron.tile_budget); },
                          [](gridadmm_config& c, double v) { c.solver.tron.tile_budget = int(v); }}},
     };

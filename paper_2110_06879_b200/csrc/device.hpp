@@ -101,7 +101,9 @@ struct BranchCfg {
     int max_cg = 32;
     double delta_floor = 1e-3;
     double limit_tighten = 0.99;
-    int lane_budget = 4;  // TRON iterations a branch may take in the lane phase (swept: 4 best)
+    int lane_budget = 4;  // lane-phase steps of a branch once the active set fits the tiles
+    int lane_cap = 16;    // lane-phase steps while the active set exceeds the tile slots (swept)
+    int tile_slots = 0;   // set by the launcher: tiles available per queue
     int tile_budget = 48; // steps in the 8-lane tile phase before the solo phase takes over (0 = off)
 };
 
@@ -126,6 +128,9 @@ void launch_y_only(const DevNet& n, const DevState& s, cudaStream_t st);
 void launch_outer(const DevNet& n, const DevState& s, double beta, double lam_min,
                   double lam_max, cudaStream_t st);
 void launch_reset_scalars(DevScalars* sc, cudaStream_t st);
+// make_state + cold_start on the device (driver.cpp:26-63, decomp.cpp:37-57).
+void launch_cold_start(const DevNet& n, const DevState& s, double rho_pq, double rho_va,
+                       double limit_tighten, cudaStream_t st);
 // max(0, max_k v[k]) with NaN skipped (driver.cpp:179-183 rho_max), as bits.
 void launch_rowmax(const double* v, int n, unsigned long long* dst, cudaStream_t st);
 // Boundary exchange of multi-part runs (partition.hpp).

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "ga_math.h"
 #include "solver.hpp"
@@ -15,6 +16,46 @@ namespace {
 void check(cudaError_t e, const char* what) {
     if (e != cudaSuccess)
         throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Process-wide pinned slots for the per-iteration scalar readback: a pinned
+// allocation per session costs milliseconds, a slot costs nothing.
+std::mutex g_pinned_mu;
+std::vector<void*> g_pinned_free;
+constexpr size_t kPinnedSlot = 256;
+
+void* pinned_slot_acquire() {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    if (g_pinned_free.empty()) {
+        char* blk = nullptr;
+        check(cudaMallocHost(&blk, 64 * kPinnedSlot), "cudaMallocHost");
+        for (int k = 0; k < 64; ++k) g_pinned_free.push_back(blk + k * kPinnedSlot);
+    }
+    void* p = g_pinned_free.back();
+    g_pinned_free.pop_back();
+    return p;
+}
+
+void pinned_slot_release(void* p) {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    g_pinned_free.push_back(p);
+}
+
+// The device's default memory pool keeps freed arenas (no release threshold),
+// so a new session / solve / tracking period reuses mapped memory instead of
+// paying cudaMalloc + cudaFree of ~100 MB.
+void retain_pool(int device) {
+    static std::mutex mu;
+    static std::vector<int> done;
+    std::lock_guard<std::mutex> lk(mu);
+    for (int d : done)
+        if (d == device) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        unsigned long long thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done.push_back(device);
 }
 
 double from_bits(unsigned long long b) {
@@ -42,12 +83,9 @@ Session::Session(const Network& net, const SolverConfig& cfg, const PartPlan* pl
     }
     trace_phase("session: stream/events");
     try {
-        upload_network();
+        upload_network();  // also places sc_ and red_ in the arena
         trace_phase("session: upload network");
-        check(cudaMalloc(&sc_, sizeof(DevScalars)), "cudaMalloc scalars");
-        check(cudaMemset(sc_, 0, sizeof(DevScalars)), "cudaMemset scalars");
-        check(cudaMallocHost(&sc_host_, sizeof(DevScalars)), "cudaMallocHost");
-        check(cudaMalloc(&red_, sizeof(unsigned long long)), "cudaMalloc red");
+        sc_host_ = static_cast<DevScalars*>(pinned_slot_acquire());
     } catch (...) {
         free_all();
         throw;
@@ -59,11 +97,10 @@ Session::~Session() { free_all(); }
 
 void Session::free_all() {
     if (stream_) cudaStreamSynchronize(stream_);
-    for (void* p : allocs_) cudaFree(p);
+    for (void* p : allocs_) cudaFreeAsync(p, stream_);  // back to the device pool
+    if (!allocs_.empty() && stream_) cudaStreamSynchronize(stream_);
     allocs_.clear();
-    if (sc_) cudaFree(sc_);
-    if (red_) cudaFree(red_);
-    if (sc_host_) cudaFreeHost(sc_host_);
+    if (sc_host_) pinned_slot_release(sc_host_);
     if (flush_buf_) cudaFree(flush_buf_);
     flush_buf_ = nullptr;
     sc_ = nullptr;
@@ -84,17 +121,26 @@ void Session::upload_network() {
     dn_.nl = nl;
     dn_.m = m;
     dn_.ref_bus = net_.ref_bus;
+    // One device arena for the whole network + state (one cudaMalloc instead
+    // of ~40); the host arrays are copied after the arena exists.
+    struct Req {
+        void** slot;
+        size_t bytes;
+    };
+    struct Put {
+        void** slot;
+        const void* src;
+        size_t bytes;
+    };
+    std::vector<Req> reqs;
+    std::vector<Put> puts;
     auto alloc = [&](auto*& p, size_t count) {
         using T = std::remove_reference_t<decltype(*p)>;
-        void* raw = nullptr;
-        check(cudaMalloc(&raw, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
-        allocs_.push_back(raw);
-        p = static_cast<T*>(raw);
+        reqs.push_back({reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T)});
     };
-    auto put = [&](auto* dst, const auto& host) {
+    auto put = [&](auto*& dst, const auto& host) {
         if (!host.empty())
-            check(cudaMemcpy(dst, host.data(), host.size() * sizeof(host[0]), cudaMemcpyHostToDevice),
-                  "cudaMemcpy H2D");
+            puts.push_back({reinterpret_cast<void**>(&dst), host.data(), host.size() * sizeof(host[0])});
     };
     // generators
     std::vector<double> pmin(ng), pmax(ng), qmin(ng), qmax(ng), c2(ng), c1(ng);
@@ -144,7 +190,9 @@ void Session::upload_network() {
     alloc(dn_.b_bs, nb); put(dn_.b_bs, bs);
     alloc(dn_.b_vmin, nb); put(dn_.b_vmin, vmin);
     alloc(dn_.b_vmax, nb); put(dn_.b_vmax, vmax);
+    trace_phase("upload: host SoA");
     const BusCsr csr = build_bus_csr(net_);
+    trace_phase("upload: bus CSR");
     alloc(dn_.bus_grp, csr.grp.size()); put(dn_.bus_grp, csr.grp);
     alloc(dn_.bus_rows, csr.rows.size()); put(dn_.bus_rows, csr.rows);
     // state
@@ -154,7 +202,6 @@ void Session::upload_network() {
     alloc(ds_.bp, 6 * static_cast<size_t>(nl));
     alloc(ds_.lt_ij, nl); alloc(ds_.lt_ji, nl); alloc(ds_.rho_t, nl);
     alloc(ds_.br_cost, nl);
-    check(cudaMemset(ds_.br_cost, 0, std::max(nl, 1) * sizeof(int)), "cudaMemset cost");
     alloc(ds_.branch_ws, branch_workspace_ints(dn_));
     alloc(ds_.mig_x, 6 * static_cast<size_t>(nl));
     alloc(ds_.mig_f, nl);
@@ -177,58 +224,36 @@ void Session::upload_network() {
             alloc(d_recv_[q], plan_.recv_x[q].size()); put(d_recv_[q], plan_.recv_x[q]);
         }
     }
+    alloc(sc_, 1);
+    alloc(red_, 1);
+    size_t total = 0;
+    for (const Req& r : reqs) total += (r.bytes + 255) & ~size_t(255);
+    void* arena = nullptr;
+    retain_pool(cfg_.device);
+    check(cudaMallocAsync(&arena, total, stream_), "cudaMallocAsync arena");
+    allocs_.push_back(arena);
+    size_t off = 0;
+    for (const Req& r : reqs) {
+        *r.slot = static_cast<char*>(arena) + off;
+        off += (r.bytes + 255) & ~size_t(255);
+    }
+    trace_phase("upload: arena");
+    for (const Put& p : puts)
+        check(cudaMemcpyAsync(*p.slot, p.src, p.bytes, cudaMemcpyHostToDevice, stream_), "H2D");
+    check(cudaMemsetAsync(ds_.br_cost, 0, std::max(nl, 1) * sizeof(int), stream_), "cudaMemset cost");
+    check(cudaMemsetAsync(sc_, 0, sizeof(DevScalars), stream_), "cudaMemset scalars");
+    check(cudaStreamSynchronize(stream_), "sync");
 }
 
-// make_state + cold_start (decomp.cpp:37-57, driver.cpp:26-63), on the host
-// (O(G + L), once per solve) then one upload.
+// make_state + cold_start (decomp.cpp:37-57, driver.cpp:26-63) on the device:
+// one kernel over rows / branches / generators / buses (branch.cu), the same
+// expressions as the reference, so no state upload is needed.
 void Session::cold_start() {
-    const int nb = net_.nb(), ng = net_.ng(), nl = net_.nl(), m = net_.m();
-    HostState s;
-    s.x.assign(m, 0.0);
-    s.xbar.assign(m, 0.0);
-    s.z.assign(m, 0.0);
-    s.y.assign(m, 0.0);
-    s.lambda.assign(m, 0.0);
-    s.rho.resize(m);
-    for (int k = 0; k < m; ++k) {
-        const bool pq = k < 2 * ng || (k - 2 * ng) % 8 < 4;
-        s.rho[k] = pq ? cfg_.rho_pq : cfg_.rho_va;
-    }
-    s.beta = cfg_.beta0;
-    s.bus_w.assign(nb, 0.0);
-    s.bus_theta.assign(nb, 0.0);
-    s.bp.assign(6 * static_cast<size_t>(nl), 0.0);
-    s.lt_ij.assign(nl, 0.0);
-    s.lt_ji.assign(nl, 0.0);
-    s.rho_t.assign(nl, cfg_.rho_pq);
-    for (int g = 0; g < ng; ++g) {
-        const Gen& gen = net_.gens[g];
-        s.x[2 * g] = s.xbar[2 * g] = 0.5 * (gen.pmin + gen.pmax);
-        s.x[2 * g + 1] = s.xbar[2 * g + 1] = 0.5 * (gen.qmin + gen.qmax);
-    }
-    for (int i = 0; i < nb; ++i) {
-        const double v = 0.5 * (net_.buses[i].vmin + net_.buses[i].vmax);
-        s.bus_w[i] = v * v;
-        s.bus_theta[i] = 0.0;
-    }
-    for (int b = 0; b < nl; ++b) {
-        const Line& br = net_.lines[b];
-        const double vi = 0.5 * (net_.buses[br.from].vmin + net_.buses[br.from].vmax);
-        const double vj = 0.5 * (net_.buses[br.to].vmin + net_.buses[br.to].vmax);
-        double* pt = &s.bp[6 * static_cast<size_t>(b)];
-        pt[0] = vi; pt[1] = vj; pt[2] = 0.0; pt[3] = 0.0; pt[4] = 0.0; pt[5] = 0.0;
-        double f[4];
-        branch_flows_host(br.y, vi, vj, 0.0, 0.0, f);
-        const double vals[8] = {f[0], f[1], f[2], f[3], vi * vi, 0.0, vj * vj, 0.0};
-        const int base = 2 * ng + 8 * b;
-        for (int k = 0; k < 8; ++k) s.x[base + k] = s.xbar[base + k] = vals[k];
-        if (br.limited()) {
-            const double rt = cfg_.limit_tighten * br.rate;
-            pt[4] = sclamp(-(f[0] * f[0] + f[1] * f[1]), -rt * rt, 0.0);
-            pt[5] = sclamp(-(f[2] * f[2] + f[3] * f[3]), -rt * rt, 0.0);
-        }
-    }
-    upload_state(s);
+    check(cudaSetDevice(cfg_.device), "cudaSetDevice");
+    launch_cold_start(dn_, ds_, cfg_.rho_pq, cfg_.rho_va, cfg_.limit_tighten, stream_);
+    check(cudaGetLastError(), "cold start launch");
+    check(cudaStreamSynchronize(stream_), "sync");
+    beta_ = cfg_.beta0;
 }
 
 void Session::upload_state(const HostState& s) {
@@ -340,6 +365,12 @@ BranchCfg branch_cfg(const SolverConfig& c) {
         return e ? std::atoi(e) : -1;
     }();
     if (tile_budget >= 0) b.tile_budget = tile_budget;
+    static const int lane_cap = [] {
+        const char* e = std::getenv("GRIDADMM_LANE_CAP");
+        return e ? std::atoi(e) : -1;
+    }();
+    if (lane_cap >= 1) b.lane_cap = lane_cap;
+    if (b.lane_cap < b.lane_budget) b.lane_cap = b.lane_budget;
     return b;
 }
 

@@ -352,7 +352,10 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
     const int tbase = lane & ~(T - 1);
     const unsigned mask = (T == 32 ? 0xffffffffu : ((1u << T) - 1u)) << tbase;
     const TileSearch<T> search{mask, tbase, rank};
-    const Slot<S> slot{smem + threadIdx.x / T};
+    // A warp only ever uses the slots of its own 32 / kTile tiles, whatever T:
+    // warps of one block may run different T (tail mode is decided per
+    // queue), and must not share a slot.
+    const Slot<S> slot{smem + (threadIdx.x / T) * (T / kTile)};
     BranchProb<N, S> p{slot};
     const TronParams tp = tron_params(cfg);
     const int count = *ovf_count;

@@ -32,13 +32,18 @@ def write_profile(net, periods, path, seed=25):
 def main():
     shape = sys.argv[1] if len(sys.argv) > 1 else "case_ACTIVSg25k"
     periods = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-    preset = sys.argv[3] if len(sys.argv) > 3 else "case_ACTIVSg25k"
+    preset = sys.argv[3] if len(sys.argv) > 3 else "case_ACTIVSg25k"  # or "rho_pq:rho_va"
     max_inner = int(sys.argv[4]) if len(sys.argv) > 4 else 1000
     max_outer = int(sys.argv[5]) if len(sys.argv) > 5 else 20
     path = synth.ensure_case(shape, "/tmp/gridadmm_cases")
     net = ga.Network(path)
     prof = write_profile(net, periods, f"/tmp/gridadmm_cases/{shape}_profile_{periods}.csv")
-    cfg = ga.Config(preset, max_inner=max_inner, max_outer=max_outer, ramp_frac=0.02)
+    if ":" in preset:
+        rpq, rva = (float(v) for v in preset.split(":"))
+        cfg = ga.Config(rho_pq=rpq, rho_va=rva, max_inner=max_inner, max_outer=max_outer,
+                        ramp_frac=0.02)
+    else:
+        cfg = ga.Config(preset, max_inner=max_inner, max_outer=max_outer, ramp_frac=0.02)
     t0 = time.perf_counter()
     st, trk = ga.track(net, cfg, prof)
     wall = time.perf_counter() - t0

@@ -190,3 +190,26 @@ def test_branch_schedule_invariance(gridadmm, oracle_mod, name, lane_budget, til
     if not z_last <= d["eps"]:
         sess.phase("outer", z_last, -1.0)
     assert_state_equal(sess.get_state(), fin, f"{name} final")
+
+
+@pytest.mark.parametrize("shape,lane_budget", [("case13659pegase", 4), ("case13659pegase", 1),
+                                               ("case2868rte", 2)])
+def test_series_parity_synthetic_scale(gridadmm, oracle_mod, shape, lane_budget):
+    """Residual series at scale (tens of thousands of branches: all three
+    branch phases, both tile widths side by side in one tile kernel, the
+    block-staged bus kernel with multi-block staging) vs the reference, for
+    two device runs with different lane budgets."""
+    from paper_2110_06879_b200 import synth
+    import os
+    iters = 30
+    path = synth.ensure_case(shape, "/tmp/gridadmm_cases")
+    net = gridadmm.Network(path)
+    cfg = gridadmm.Config(rho_pq=100.0, rho_va=1e4)
+    cfg["lane_budget"] = lane_budget
+    sess = gridadmm.Session(net, cfg)
+    rec, _ = sess.iterate(iters)
+    ref = oracle_mod.RefNet(path)
+    series, _, _ = ref.solve(rho_pq=100.0, rho_va=1e4, max_outer=1, max_inner=iters,
+                             workers=os.cpu_count() or 1)
+    assert len(rec) == len(series) == iters
+    assert_bits_equal(rec[:, 0:3], series[:, 2:5], f"{shape} residuals")

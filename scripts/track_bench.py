@@ -15,16 +15,16 @@ import paper_2110_06879_b200 as ga  # noqa: E402
 from paper_2110_06879_b200 import synth  # noqa: E402
 
 
-def write_profile(net, periods, path, seed=25):
+def write_profile(net, periods, path, seed=25, swing=0.05, noise=0.005):
     rng = np.random.default_rng(seed)
     ids = net.export()["bus_id"]
-    hourly = 1.0 + 0.05 * np.sin(np.linspace(0.0, np.pi, 4))  # <= 5% swing
+    hourly = 1.0 + swing * np.sin(np.linspace(0.0, np.pi, 4))  # <= 5% swing
     t = np.linspace(0, len(hourly) - 1, periods)
     level = np.interp(t, np.arange(len(hourly)), hourly) / hourly[0]
     with open(path, "w") as f:
         f.write("period,bus,multiplier\n")
         for p in range(periods):
-            m = level[p] * (1.0 + 0.005 * rng.standard_normal(len(ids)))
+            m = level[p] * (1.0 + noise * rng.standard_normal(len(ids)))
             f.write("".join(f"{p + 1},{i},{v:.9f}\n" for i, v in zip(ids, m)))
     return path
 
@@ -35,9 +35,12 @@ def main():
     preset = sys.argv[3] if len(sys.argv) > 3 else "case_ACTIVSg25k"  # or "rho_pq:rho_va"
     max_inner = int(sys.argv[4]) if len(sys.argv) > 4 else 1000
     max_outer = int(sys.argv[5]) if len(sys.argv) > 5 else 20
+    swing = float(sys.argv[6]) if len(sys.argv) > 6 else 0.05
+    noise = float(sys.argv[7]) if len(sys.argv) > 7 else 0.005
     path = synth.ensure_case(shape, "/tmp/gridadmm_cases")
     net = ga.Network(path)
-    prof = write_profile(net, periods, f"/tmp/gridadmm_cases/{shape}_profile_{periods}.csv")
+    prof = write_profile(net, periods, f"/tmp/gridadmm_cases/{shape}_profile_{periods}.csv",
+                         swing=swing, noise=noise)
     if ":" in preset:
         rpq, rva = (float(v) for v in preset.split(":"))
         cfg = ga.Config(rho_pq=rpq, rho_va=rva, max_inner=max_inner, max_outer=max_outer,
@@ -55,7 +58,8 @@ def main():
         per.append({"period": int(r["period"]), "inner": int(r["inner_iters"]),
                     "time_s": float(r["time_s"]), "c_inf": float(r["viol_inf"])})
     warm = [p["time_s"] for p in per[1:]]
-    out = {"shape": shape, "periods": periods, "preset": preset, "status": ga.STATUS[st],
+    out = {"shape": shape, "periods": periods, "preset": preset, "swing": swing, "noise": noise,
+           "status": ga.STATUS[st],
            "wall_s": wall, "cold_s": per[0]["time_s"] if per else None,
            "warm_s_per_step_mean": float(np.mean(warm)) if warm else None,
            "warm_s_per_step_max": float(np.max(warm)) if warm else None,

@@ -196,107 +196,35 @@ GA_FN void cauchy_point(const double* x, const double* g, const HM& h,
         if (!(vnorm2<N>(st) <= delta)) return false;
         return model<N>(g, h, st) <= kTronMu0 * vdot<N>(g, st);
     };
-    double alpha = smin(1.0, delta / gnorm);
-    step_at(alpha, s);
-    if (ok(s)) {
-        double trial[N];
-        for (int it = 0; it < 20; ++it) {
+    // One trial site (instruction-cache footprint: this is the hottest loop of
+    // the lane phase, ~21 trials per step): phase 0 is alpha0, phase 1 the
+    // extrapolation (tron.cpp:115-124: continue from the last accepted
+    // alpha, at most 20 doublings), phase 2 the backtracking (tron.cpp:127-
+    // 135: at most 40 halvings, first success wins, else the last trial).
+    double a = smin(1.0, delta / gnorm);
+    int phase = 0, cnt = 0;
+    double t[N];
+    for (;;) {
+        step_at(a, t);
+        const bool o = ok(t);
+        if (phase == 0) {
+            phase = o ? 1 : 2;
+        } else if (phase == 1) {
+            if (!o) return;
+        }
+#pragma unroll
+        for (int i = 0; i < N; ++i) s[i] = t[i];
+        if (phase == 2 && o && cnt > 0) return;
+        if (phase == 1) {
+            if (cnt >= 20) return;
             GA_STAT(1);
-            const double next = alpha * 2.0;
-            step_at(next, trial);
-            if (!ok(trial)) break;
-            alpha = next;
-#pragma unroll
-            for (int i = 0; i < N; ++i) s[i] = trial[i];
-        }
-        return;
-    }
-    for (int it = 0; it < 40; ++it) {
-        GA_STAT(2);
-        alpha *= 0.5;
-        step_at(alpha, s);
-        if (ok(s)) return;
-    }
-}
-
-// Cauchy point with the backtracking trials evaluated B at a time.
-//
-// The reference's backtracking (tron.cpp:127-135) tries alpha0 * 2^-k for
-// k = 1..40 and stops at the first success; on the 70k-shaped grids it runs
-// ~21 trials per TRON iteration (alpha0 = 1 against Hessian eigenvalues
-// ~1e6), each a short dependent chain (clamp, norm, model).  The trials are
-// independent of each other, so one thread evaluates B consecutive ones side
-// by side (instruction-level parallelism) and takes the first success of the
-// batch — the trial the sequential loop stops at.  Round 0 speculatively
-// evaluates k = 0..B-1; if k = 0 succeeds the extrapolation branch runs
-// exactly as in cauchy_point.  Every trial uses the sequential loop's
-// expressions (alpha halved step by step), so the result is bit-identical.
-template <int N, int B, class HM>
-GA_FN void cauchy_point_batched(const double* x, const double* g, const HM& h,
-                                const double* l, const double* u, double delta, double* s) {
-    const double gnorm = vnorm2<N>(g);
-    if (gnorm == 0.0) {
-#pragma unroll
-        for (int i = 0; i < N; ++i) s[i] = 0.0;
-        return;
-    }
-    auto step_at = [&](double alpha, double* out) {
-#pragma unroll
-        for (int i = 0; i < N; ++i) out[i] = sclamp(x[i] - alpha * g[i], l[i], u[i]) - x[i];
-    };
-    auto ok = [&](const double* st) {
-        const bool in_region = vnorm2<N>(st) <= delta;
-        return in_region && model<N>(g, h, st) <= kTronMu0 * vdot<N>(g, st);
-    };
-    const double alpha0 = smin(1.0, delta / gnorm);
-    double a = alpha0;  // alpha of the next trial to form
-    for (int k0 = 0; k0 <= 40; k0 += B) {
-        double tr[B][N];
-        bool okb[B];
-        // branch-free over the batch so the B chains interleave
-        double nrm[B], mdl[B], gts[B];
-#pragma unroll
-        for (int b = 0; b < B; ++b) {
-            if (k0 + b > 0) a *= 0.5;  // trial k = k0 + b at alpha0 * 2^-k
-            step_at(a, tr[b]);
-        }
-#pragma unroll
-        for (int b = 0; b < B; ++b) nrm[b] = vdot<N>(tr[b], tr[b]);
-#pragma unroll
-        for (int b = 0; b < B; ++b) gts[b] = vdot<N>(g, tr[b]);
-#pragma unroll
-        for (int b = 0; b < B; ++b) mdl[b] = model<N>(g, h, tr[b]);
-#pragma unroll
-        for (int b = 0; b < B; ++b)
-            okb[b] = (k0 + b <= 40) & (sqrt(nrm[b]) <= delta) & (mdl[b] <= kTronMu0 * gts[b]);
-        if (k0 == 0 && okb[0]) {
-            // alpha0 accepted: extrapolate (tron.cpp:115-124)
-            double alpha = alpha0;
-#pragma unroll
-            for (int i = 0; i < N; ++i) s[i] = tr[0][i];
-            double trial[N];
-            for (int it = 0; it < 20; ++it) {
-                GA_STAT(1);
-                const double next = alpha * 2.0;
-                step_at(next, trial);
-                if (!ok(trial)) break;
-                alpha = next;
-#pragma unroll
-                for (int i = 0; i < N; ++i) s[i] = trial[i];
-            }
-            return;
-        }
-#pragma unroll
-        for (int b = 0; b < B; ++b) {
-            const int k = k0 + b;
-            if (k == 0 || k > 40) continue;
+            a = a * 2.0;
+        } else {
+            if (cnt >= 40) return;
             GA_STAT(2);
-            if (okb[b] || k == 40) {  // first success, or the last trial's step
-#pragma unroll
-                for (int i = 0; i < N; ++i) s[i] = tr[b][i];
-                return;
-            }
+            a *= 0.5;
         }
+        ++cnt;
     }
 }
 
@@ -462,16 +390,12 @@ struct HessSmem {
 #endif
 
 // Sequential search strategy (one thread per solve): the reference's loops.
-#ifndef GA_CAUCHY_B
-#define GA_CAUCHY_B 1
-#endif
 struct SerialSearch {
     static constexpr bool kClocked = false;
     template <int N, class HM>
     GA_FN void cauchy(const double* x, const double* g, const HM& h, const double* l,
                       const double* u, double delta, double* s) const {
-        if constexpr (GA_CAUCHY_B > 1) cauchy_point_batched<N, GA_CAUCHY_B>(x, g, h, l, u, delta, s);
-        else cauchy_point<N>(x, g, h, l, u, delta, s);
+        cauchy_point<N>(x, g, h, l, u, delta, s);
     }
     // Projected line search on s + beta d (tron.cpp:279-291); returns the step.
     template <int N, class HM>

@@ -419,6 +419,20 @@ def run_b200(args, d: Dist):
     except Exception:
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    # DRAM traffic per launch of the dominant kernel from the committed ncu
+    # --set full capture (profiles/r01_ncu_traffic.jsonl, inner iteration 10)
+    traffic, traffic_note = None, None
+    try:
+        unit = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        for ln in open(os.path.join(REPO, "profiles", "r01_ncu_traffic.jsonl")):
+            t = json.loads(ln)
+            if t["kernel"] == "lane_kernel":
+                traffic = t["dram_read"][0] * unit[t["dram_read"][1]] + \
+                    t["dram_write"][0] * unit[t["dram_write"][1]]
+                traffic_note = ("lane_kernel dram__bytes_read+write per launch, ncu --set full, "
+                                "profiles/r01_ncu_traffic.jsonl; the phase is FP64-latency bound")
+    except Exception:  # noqa: BLE001
+        pass
 
     # --- e2e through the C ABI (host buffers) -----------------------------
     e2e = None
@@ -487,7 +501,7 @@ def run_b200(args, d: Dist):
                          "kernel": "branch phase: lane_kernel + tile_kernel + solo_kernel (TRON NLPs)",
                          "achieved": achieved, "peak": fp64_mul_add, "unit": "TFLOP/s",
                          "frac": achieved / fp64_mul_add if fp64_mul_add else None,
-                         "traffic": None,
+                         "traffic": traffic, "traffic_note": traffic_note,
                          "peak_note": "measured DMUL+DADD issue rate (kernel built -fmad=false); "
                                       f"DFMA peak {fp64_fma:.1f} TFLOP/s",
                          "flops_per_launch": flops / max(1, kern["branches"]["launches"]),

@@ -81,6 +81,32 @@ GA_FN long long __double_as_longlong_portable(double v) {
 #endif
 }
 
+// IEEE division / square root, inline or at one out-of-line site each.  The
+// unrolled Cholesky factor and solves hold ~50 copies of each ~20-instruction
+// sequence.  The lane phase (one branch per thread, top stall: instruction
+// fetch on a 180 KB kernel) calls them out of line: lane phase -5% in the
+// bench window, -12% over a full 70k solve.  The tile / solo phases (one
+// branch per 8 or 32 lanes, latency-bound chains) keep them inline: out of
+// line they were 5-9% slower.  Same IEEE operations either way.
+#if defined(__CUDA_ARCH__)
+__device__ __noinline__ double ga_div_ool(double a, double b) { return a / b; }
+__device__ __noinline__ double ga_sqrt_ool(double a) { return sqrt(a); }
+#endif
+template <bool kOol>
+GA_FN double tdiv(double a, double b) {
+#if defined(__CUDA_ARCH__)
+    if constexpr (kOol) return ga_div_ool(a, b);
+#endif
+    return a / b;
+}
+template <bool kOol>
+GA_FN double tsqrt(double a) {
+#if defined(__CUDA_ARCH__)
+    if constexpr (kOol) return ga_sqrt_ool(a);
+#endif
+    return sqrt(a);
+}
+
 // ---- sequential reductions over N (tron.cpp:16-51) ------------------------
 
 template <int N>
@@ -120,7 +146,7 @@ GA_FN double mdot(unsigned fm, const double* a, const double* b) {
 
 // Cholesky of the free principal submatrix (tron.cpp:53-67): reads the lower
 // triangle h[i][j], i > j, as the reference's hf does.
-template <int N, class HM>
+template <int N, bool kOol, class HM>
 GA_FN bool mcholesky(unsigned fm, const HM& h, double* L) {
 #pragma unroll
     for (int j = 0; j < N; ++j) {
@@ -130,7 +156,7 @@ GA_FN bool mcholesky(unsigned fm, const HM& h, double* L) {
         for (int k = 0; k < j; ++k)
             if (fm >> k & 1u) d -= L[j * N + k] * L[j * N + k];
         if (d <= 0.0 || !sfinite(d)) return false;
-        L[j * N + j] = sqrt(d);
+        L[j * N + j] = tsqrt<kOol>(d);
 #pragma unroll
         for (int i = j + 1; i < N; ++i) {
             if (!(fm >> i & 1u)) continue;
@@ -138,14 +164,14 @@ GA_FN bool mcholesky(unsigned fm, const HM& h, double* L) {
 #pragma unroll
             for (int k = 0; k < j; ++k)
                 if (fm >> k & 1u) v -= L[i * N + k] * L[j * N + k];
-            L[i * N + j] = v / L[j * N + j];
+            L[i * N + j] = tdiv<kOol>(v, L[j * N + j]);
         }
     }
     return true;
 }
 
 // (L L')^{-1} b on the free set (tron.cpp:69-80).
-template <int N>
+template <int N, bool kOol>
 GA_FN void mchol_solve(unsigned fm, const double* L, const double* b, double* x) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -154,7 +180,7 @@ GA_FN void mchol_solve(unsigned fm, const double* L, const double* b, double* x)
 #pragma unroll
         for (int k = 0; k < i; ++k)
             if (fm >> k & 1u) v -= L[i * N + k] * x[k];
-        x[i] = v / L[i * N + i];
+        x[i] = tdiv<kOol>(v, L[i * N + i]);
     }
 #pragma unroll
     for (int i = N - 1; i >= 0; --i) {
@@ -163,7 +189,7 @@ GA_FN void mchol_solve(unsigned fm, const double* L, const double* b, double* x)
 #pragma unroll
         for (int k = i + 1; k < N; ++k)
             if (fm >> k & 1u) v -= L[k * N + i] * x[k];
-        x[i] = v / L[i * N + i];
+        x[i] = tdiv<kOol>(v, L[i * N + i]);
     }
 }
 
@@ -230,7 +256,7 @@ GA_FN void cauchy_point(const double* x, const double* g, const HM& h,
 
 // Preconditioned Steihaug CG on the free subspace at x + s
 // (tron.cpp:141-224).  d receives the full-space correction.
-template <int N, class HM>
+template <int N, bool kOol, class HM>
 GA_FN void subspace_cg(const double* x, const double* g, const HM& h,
                        const double* l, const double* u, double delta,
                        const TronParams& cfg, const double* s, double* d) {
@@ -253,7 +279,7 @@ GA_FN void subspace_cg(const double* x, const double* g, const HM& h,
         rf[i] = -(g[i] + hs);
         dk[i] = 0.0;
     }
-    const bool have_prec = mcholesky<N>(fm, h, L);
+    const bool have_prec = mcholesky<N, kOol>(fm, h, L);
     if (!have_prec) GA_STAT(5);
     double rz = 0.0, r0 = 0.0;
     // it = -1 is the set-up (z0 = M^-1 r0, p0 = z0); the preconditioner solve
@@ -308,7 +334,7 @@ GA_FN void subspace_cg(const double* x, const double* g, const HM& h,
             }
         if (sqrt(mdot<N>(fm, rf, rf)) <= cfg.cg_tol * r0) break;
       }
-        if (have_prec) mchol_solve<N>(fm, L, rf, zk);
+        if (have_prec) mchol_solve<N, kOol>(fm, L, rf, zk);
         else {
 #pragma unroll
             for (int i = 0; i < N; ++i) zk[i] = rf[i];
@@ -392,6 +418,7 @@ struct HessSmem {
 // Sequential search strategy (one thread per solve): the reference's loops.
 struct SerialSearch {
     static constexpr bool kClocked = false;
+    static constexpr bool kOolDivSqrt = true;
     template <int N, class HM>
     GA_FN void cauchy(const double* x, const double* g, const HM& h, const double* l,
                       const double* u, double delta, double* s) const {
@@ -428,6 +455,7 @@ struct SerialSearch {
 template <int T>
 struct TileSearch {
     static constexpr bool kClocked = T == 32;
+    static constexpr bool kOolDivSqrt = false;
     unsigned mask;  // warp lanes of this tile
     int base;       // first warp lane of the tile
     int rank;       // lane within the tile
@@ -557,7 +585,7 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
     GA_CLK(1);
     search.template cauchy<N>(st.x, g, h, l, u, st.delta, s);
     GA_CLK(2);
-    subspace_cg<N>(st.x, g, h, l, u, st.delta, cfg, s, d);
+    subspace_cg<N, Search::kOolDivSqrt>(st.x, g, h, l, u, st.delta, cfg, s, d);
     GA_CLK(3);
 
     const double qc = model<N>(g, h, s);

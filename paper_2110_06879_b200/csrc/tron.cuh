@@ -117,8 +117,8 @@ GA_FN double vdot(const double* a, const double* b) {
     return s;
 }
 
-template <int N>
-GA_FN double vnorm2(const double* a) { return sqrt(vdot<N>(a, a)); }
+template <int N, bool kOol = false>
+GA_FN double vnorm2(const double* a) { return tsqrt<kOol>(vdot<N>(a, a)); }
 
 // q(s) = g's + sum_i 0.5*s_i*(H s)_i  (tron.cpp:35-43)
 template <int N, class HM>
@@ -194,21 +194,21 @@ GA_FN void mchol_solve(unsigned fm, const double* L, const double* b, double* x)
 }
 
 // Largest tau >= 0 with ||s + tau p|| = delta (tron.cpp:83-90), full space.
-template <int N>
+template <int N, bool kOol = false>
 GA_FN double boundary_tau(const double* s, const double* p, double delta) {
     const double pp = vdot<N>(p, p);
     if (pp <= 0.0) return 0.0;
     const double sp = vdot<N>(s, p);
     const double ss = vdot<N>(s, s);
     const double disc = smax(0.0, sp * sp + pp * (delta * delta - ss));
-    return (-sp + sqrt(disc)) / pp;
+    return tdiv<kOol>(-sp + tsqrt<kOol>(disc), pp);
 }
 
 // Cauchy point (tron.cpp:101-137).
-template <int N, class HM>
+template <int N, bool kOol, class HM>
 GA_FN void cauchy_point(const double* x, const double* g, const HM& h,
                         const double* l, const double* u, double delta, double* s) {
-    const double gnorm = vnorm2<N>(g);
+    const double gnorm = vnorm2<N, kOol>(g);
     if (gnorm == 0.0) {
 #pragma unroll
         for (int i = 0; i < N; ++i) s[i] = 0.0;
@@ -219,7 +219,7 @@ GA_FN void cauchy_point(const double* x, const double* g, const HM& h,
         for (int i = 0; i < N; ++i) out[i] = sclamp(x[i] - alpha * g[i], l[i], u[i]) - x[i];
     };
     auto ok = [&](const double* st) {
-        if (!(vnorm2<N>(st) <= delta)) return false;
+        if (!(vnorm2<N, kOol>(st) <= delta)) return false;
         return model<N>(g, h, st) <= kTronMu0 * vdot<N>(g, st);
     };
     // One trial site (instruction-cache footprint: this is the hottest loop of
@@ -227,7 +227,7 @@ GA_FN void cauchy_point(const double* x, const double* g, const HM& h,
     // extrapolation (tron.cpp:115-124: continue from the last accepted
     // alpha, at most 20 doublings), phase 2 the backtracking (tron.cpp:127-
     // 135: at most 40 halvings, first success wins, else the last trial).
-    double a = smin(1.0, delta / gnorm);
+    double a = smin(1.0, tdiv<kOol>(delta, gnorm));
     int phase = 0, cnt = 0;
     double t[N];
     for (;;) {
@@ -305,13 +305,13 @@ GA_FN void subspace_cg(const double* x, const double* g, const HM& h,
             sd[i] = s[i] + (fr ? dk[i] : 0.0);
         }
         if (curv <= 0.0) {  // negative curvature: to the boundary
-            const double tau = boundary_tau<N>(sd, pfull, delta);
+            const double tau = boundary_tau<N, kOol>(sd, pfull, delta);
 #pragma unroll
             for (int i = 0; i < N; ++i)
                 if (fm >> i & 1u) dk[i] += tau * pk[i];
             break;
         }
-        const double alpha = rz / curv;
+        const double alpha = tdiv<kOol>(rz, curv);
         double dnext[N], snext[N];
 #pragma unroll
         for (int i = 0; i < N; ++i) {
@@ -319,8 +319,8 @@ GA_FN void subspace_cg(const double* x, const double* g, const HM& h,
             dnext[i] = dk[i] + alpha * pk[i];
             snext[i] = s[i] + (fr ? dnext[i] : 0.0);
         }
-        if (vnorm2<N>(snext) >= delta) {
-            const double tau = boundary_tau<N>(sd, pfull, delta);
+        if (vnorm2<N, kOol>(snext) >= delta) {
+            const double tau = boundary_tau<N, kOol>(sd, pfull, delta);
 #pragma unroll
             for (int i = 0; i < N; ++i)
                 if (fm >> i & 1u) dk[i] += tau * pk[i];
@@ -332,7 +332,7 @@ GA_FN void subspace_cg(const double* x, const double* g, const HM& h,
                 dk[i] = dnext[i];
                 rf[i] -= alpha * hpk[i];
             }
-        if (sqrt(mdot<N>(fm, rf, rf)) <= cfg.cg_tol * r0) break;
+        if (tsqrt<kOol>(mdot<N>(fm, rf, rf)) <= cfg.cg_tol * r0) break;
       }
         if (have_prec) mchol_solve<N, kOol>(fm, L, rf, zk);
         else {
@@ -344,10 +344,10 @@ GA_FN void subspace_cg(const double* x, const double* g, const HM& h,
 #pragma unroll
             for (int i = 0; i < N; ++i) pk[i] = zk[i];
             rz = rznext;
-            r0 = sqrt(mdot<N>(fm, rf, rf));
+            r0 = tsqrt<kOol>(mdot<N>(fm, rf, rf));
             if (r0 == 0.0) return;
         } else {
-            const double betak = rznext / rz;
+            const double betak = tdiv<kOol>(rznext, rz);
 #pragma unroll
             for (int i = 0; i < N; ++i)
                 if (fm >> i & 1u) pk[i] = zk[i] + betak * pk[i];
@@ -422,7 +422,7 @@ struct SerialSearch {
     template <int N, class HM>
     GA_FN void cauchy(const double* x, const double* g, const HM& h, const double* l,
                       const double* u, double delta, double* s) const {
-        cauchy_point<N>(x, g, h, l, u, delta, s);
+        cauchy_point<N, kOolDivSqrt>(x, g, h, l, u, delta, s);
     }
     // Projected line search on s + beta d (tron.cpp:279-291); returns the step.
     template <int N, class HM>
@@ -579,7 +579,8 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
 #pragma unroll
         for (int i = 0; i < N * N; ++i) h.put(i, hr[i]);
     }
-    if (st.iter == 0 && st.delta == 0.0) st.delta = smax(vnorm2<N>(g), cfg.delta_floor);
+    constexpr bool kOol = Search::kOolDivSqrt;
+    if (st.iter == 0 && st.delta == 0.0) st.delta = smax(vnorm2<N, kOol>(g), cfg.delta_floor);
 
     double s[N], d[N];
     GA_CLK(1);
@@ -601,8 +602,8 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
     if (!sfinite(ft)) return kStepError;
     const double ared = st.f - ft;
     const double pred = -q;
-    const double ratio = pred > 0.0 ? ared / pred : (ared > 0.0 ? 1.0 : -1.0);
-    const double snorm = vnorm2<N>(stp);
+    const double ratio = pred > 0.0 ? tdiv<kOol>(ared, pred) : (ared > 0.0 ? 1.0 : -1.0);
+    const double snorm = vnorm2<N, kOol>(stp);
     const double delta_used = st.delta;
     if (ratio < 0.25) st.delta = 0.25 * smax(snorm, 1e-12);
     else if (ratio > 0.75 && snorm >= 0.9 * st.delta) st.delta = smin(2.0 * st.delta, kTronDeltaMax);

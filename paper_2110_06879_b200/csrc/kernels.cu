@@ -518,8 +518,11 @@ __global__ void __launch_bounds__(kBusWarps * 32) bus_warp_kernel(DevNet n, DevS
 // Fusing z / y is exact: every row is consumed by exactly one bus
 // (proj/tests/test_decomp.cpp:59-71) and z / y of a row depend only on that
 // row, so the order "all buses, then all z, then all y" is not observable.
-constexpr int kBB = 128;
-constexpr int kStage = 2048;  // staged rows per block; the rest are read from global
+#ifndef GA_BUS_BLOCK
+#define GA_BUS_BLOCK 128
+#endif
+constexpr int kBB = GA_BUS_BLOCK;  // buses (threads) per block
+constexpr int kStage = 16 * kBB;   // staged rows per block; the rest are read from global
 
 // largest slot with off[slot] <= p  (off[0] = 0 <= p < off[kBB])
 __device__ __forceinline__ int find_slot(const int* off, int p) {

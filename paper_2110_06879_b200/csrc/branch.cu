@@ -523,6 +523,7 @@ struct QpProb {
     GA_FN void hessian(const double*, double* h) const {
         for (int i = 0; i < N * N; ++i) h[i] = H[i];
     }
+    GA_FN double hess_entry(const double*, int i, int j) const { return H[i * N + j]; }
 };
 
 // One QP per thread (SerialSearch) or per tile of T lanes (TileSearch) —

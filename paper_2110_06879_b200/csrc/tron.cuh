@@ -419,6 +419,8 @@ struct HessSmem {
 struct SerialSearch {
     static constexpr bool kClocked = false;
     static constexpr bool kOolDivSqrt = true;
+    template <int N, class P>
+    GA_FN void hessian(const P& prob, const double* x, double* h) const { prob.hessian(x, h); }
     template <int N, class HM>
     GA_FN void cauchy(const double* x, const double* g, const HM& h, const double* l,
                       const double* u, double delta, double* s) const {
@@ -453,9 +455,31 @@ struct SerialSearch {
 // computed exactly as the sequential loop computes it (scaling by powers of
 // two is exact), so the selected step is bit-identical.
 template <int T>
+#ifndef GA_TILE_HESS
+#define GA_TILE_HESS 0  // measured slower
+#endif
 struct TileSearch {
     static constexpr bool kClocked = T == 32;
     static constexpr bool kOolDivSqrt = false;
+    // The tile's lanes split the N*N Hessian entries (each computed with the
+    // serial evaluation's exact operation sequence, P::hess_entry) and
+    // exchange them with shuffles: every lane ends with the full matrix.
+    template <int N, class P>
+    __device__ void hessian(const P& prob, const double* x, double* h) const {
+        if constexpr (!GA_TILE_HESS) {
+            prob.hessian(x, h);
+        } else {
+            constexpr int E = N * N, M = (E + T - 1) / T;
+            double mine[M];
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+                const int e = rank + m * T;
+                mine[m] = e < E ? prob.hess_entry(x, e / N, e % N) : 0.0;
+            }
+#pragma unroll
+            for (int e = 0; e < E; ++e) h[e] = __shfl_sync(mask, mine[e / T], e % T, T);
+        }
+    }
     unsigned mask;  // warp lanes of this tile
     int base;       // first warp lane of the tile
     int rank;       // lane within the tile
@@ -572,7 +596,7 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
     auto h = prob.template hess_store<N>();
     {
         double hr[N * N];
-        prob.hessian(st.x, hr);
+        search.template hessian<N>(prob, st.x, hr);
 #pragma unroll
         for (int i = 0; i < N * N; ++i)
             if (!sfinite(hr[i])) return kStepError;

@@ -337,6 +337,9 @@ __global__ void __launch_bounds__(kLaneBlock, GA_LANE_MINB) lane_kernel(DevNet n
 }
 
 // ---- phase B: tiles of kTile lanes per overflow branch ---------------------
+#ifndef GA_GH_CACHE
+#define GA_GH_CACHE 0  // tile / solo: reuse gradient + Hessian after rejected steps (measured slower)
+#endif
 // Budget > 0: a branch still running after `budget` steps here is saved and
 // pushed to the solo queue (solo / solo_count), resumed by the solo phase.
 template <int N, int T>
@@ -356,7 +359,7 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
     // warps of one block may run different T (tail mode is decided per
     // queue), and must not share a slot.
     const Slot<S> slot{smem + (threadIdx.x / T) * (T / kTile)};
-    BranchProb<N, S> p{slot};
+    BranchProb<N, S, false, GA_GH_CACHE != 0> p{slot};
     const TronParams tp = tron_params(cfg);
     const int count = *ovf_count;
     unsigned long long my_iters = 0;
@@ -374,6 +377,7 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
         ts.f = st.mig_f[b];
         ts.delta = st.mig_delta[b];
         ts.iter = st.mig_iter[b];
+        ts.ghc = false;  // the cache slot may hold another branch's values
         int al_it = st.mig_al[b];
         double prev_res = st.mig_prev_res[b];
         int iters = st.mig_cost[b];
@@ -432,7 +436,7 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
 
 __global__ void __launch_bounds__(kTileBlock, GA_TILE_MINB) tile_kernel(DevNet net, DevState st, BranchCfg cfg,
                                                           Work w, DevScalars* sc) {
-    __shared__ double smem[kFields * (kTileBlock / kTile)];
+    __shared__ double smem[(GA_GH_CACHE ? kFieldsCache : kFields) * (kTileBlock / kTile)];
     unsigned long long it6 = 0, it4 = 0;
     int fails = 0;
     // Tail mode: when a queue holds no more branches than half the grid's
@@ -482,7 +486,7 @@ __global__ void __launch_bounds__(kTileBlock, GA_TILE_MINB) tile_kernel(DevNet n
 // diverging in the warp) in a block of its own.
 __global__ void __launch_bounds__(kSoloBlock) solo_kernel(DevNet net, DevState st, BranchCfg cfg,
                                                           Work w, DevScalars* sc) {
-    __shared__ double smem[kFields * (kTileBlock / kTile)];
+    __shared__ double smem[(GA_GH_CACHE ? kFieldsCache : kFields) * (kTileBlock / kTile)];
     unsigned long long it6 = 0, it4 = 0;
     int fails = 0;
     tile_phase<6, 32>(net, st, cfg, w.solo6, &w.ctr[6], &w.ctr[8], smem, &it6, &fails, &sc->exec6, 0,
@@ -499,6 +503,11 @@ __global__ void __launch_bounds__(kSoloBlock) solo_kernel(DevNet net, DevState s
 // Dense box QP for the TRON-core parity test (proj/tests/acceptance.cpp:458-520).
 template <int N>
 struct QpProb {
+    static constexpr bool kGhCache = false;
+    GA_FN double cache_g(int) const { return 0.0; }
+    GA_FN double cache_h(int) const { return 0.0; }
+    GA_FN void cache_put_g(int, double) const {}
+    GA_FN void cache_put_h(int, double) const {}
     const double *H, *G, *L, *U;
     template <int NN>
     GA_FN HessRegs<NN> hess_store() const { return HessRegs<NN>{}; }

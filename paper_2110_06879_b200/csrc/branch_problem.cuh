@@ -38,8 +38,11 @@ enum Field : int {
     F_LTIJ = 40, F_LTJI = 41, F_RHOT = 42,
     F_VMIN_I = 43, F_VMAX_I = 44, F_VMIN_J = 45, F_VMAX_J = 46, F_R2 = 47,
     kFields = 48,
-    F_H = 48,            // lane phase: the TRON Hessian, 36 fields (HessSmem)
-    kFieldsHess = 84
+    F_H = 48,            // lane phase: the TRON Hessian, 36 fields (HessSmem);
+                         // tile / solo phases: the cached Hessian (kGhCache)
+    kFieldsHess = 84,
+    F_GC = 84,           // tile / solo phases: the cached gradient, 6 fields
+    kFieldsCache = 90
 };
 
 // One branch's data: field f of slot s lives at smem[f * S + s].
@@ -161,9 +164,14 @@ struct YcView {
 
 // The branch subproblem over a shared-memory slot (kernels.cpp:17-163).
 // kHessSmem: the TRON Hessian lives in the slot's F_H fields (lane phase).
-template <int N, int S, bool kHessSmem = false>
+template <int N, int S, bool kHessSmem = false, bool kCache = false>
 struct BranchProb {
     static constexpr bool kLimited = N == 6;
+    static constexpr bool kGhCache = kCache;  // gradient / Hessian kept across rejected steps
+    __device__ __forceinline__ double cache_g(int i) const { return s(F_GC + i); }
+    __device__ __forceinline__ double cache_h(int k) const { return s(F_H + k); }
+    __device__ __forceinline__ void cache_put_g(int i, double v) const { s.set(F_GC + i, v); }
+    __device__ __forceinline__ void cache_put_h(int k, double v) const { s.set(F_H + k, v); }
     Slot<S> s;
     mutable double cc_, ss_;  // sincos at the last gradient point
 

@@ -381,6 +381,11 @@ struct TronState {
     double f;
     double delta;
     int iter;
+    // x (and the problem data) unchanged since the gradient / Hessian were
+    // last computed, i.e. the last step was rejected: with a problem that
+    // keeps a copy (P::kGhCache) they are reloaded instead of recomputed —
+    // the same bits, since the evaluation is deterministic.
+    bool ghc;
 };
 
 // Starts a solve: clip x into the box and evaluate f (tron.cpp:235-240).
@@ -392,6 +397,7 @@ GA_FN bool tron_begin(const P& prob, TronState<N>& st) {
     st.f = prob.value(st.x);
     st.delta = 0.0;
     st.iter = 0;
+    st.ghc = false;
     return sfinite(st.f);
 }
 
@@ -586,8 +592,15 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
 #pragma unroll
     for (int i = 0; i < N; ++i) { l[i] = prob.lo(i); u[i] = prob.hi(i); }
     GA_CLK_DECL
+    constexpr bool kCache = P::kGhCache;
+    const bool cached = kCache && st.ghc;
     double g[N];
-    prob.gradient(st.x, g);
+    if (cached) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) g[i] = prob.cache_g(i);
+    } else {
+        prob.gradient(st.x, g);
+    }
 #pragma unroll
     for (int i = 0; i < N; ++i)
         if (!sfinite(g[i])) return kStepError;
@@ -596,10 +609,21 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
     auto h = prob.template hess_store<N>();
     {
         double hr[N * N];
-        search.template hessian<N>(prob, st.x, hr);
+        if (cached) {
 #pragma unroll
-        for (int i = 0; i < N * N; ++i)
-            if (!sfinite(hr[i])) return kStepError;
+            for (int i = 0; i < N * N; ++i) hr[i] = prob.cache_h(i);
+        } else {
+            search.template hessian<N>(prob, st.x, hr);
+#pragma unroll
+            for (int i = 0; i < N * N; ++i)
+                if (!sfinite(hr[i])) return kStepError;
+            if constexpr (kCache) {
+#pragma unroll
+                for (int i = 0; i < N; ++i) prob.cache_put_g(i, g[i]);
+#pragma unroll
+                for (int i = 0; i < N * N; ++i) prob.cache_put_h(i, hr[i]);
+            }
+        }
 #pragma unroll
         for (int i = 0; i < N * N; ++i) h.put(i, hr[i]);
     }
@@ -632,6 +656,7 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
     if (ratio < 0.25) st.delta = 0.25 * smax(snorm, 1e-12);
     else if (ratio > 0.75 && snorm >= 0.9 * st.delta) st.delta = smin(2.0 * st.delta, kTronDeltaMax);
     const bool accepted = ared > 0.0 && ratio > kTronEta;
+    st.ghc = !accepted;
     if (accepted) {
 #pragma unroll
         for (int i = 0; i < N; ++i) st.x[i] = xt[i];

@@ -207,7 +207,9 @@ GA_FN double boundary_tau(const double* s, const double* p, double delta) {
 // Cauchy point (tron.cpp:101-137).
 template <int N, bool kOol, class HM>
 GA_FN void cauchy_point(const double* x, const double* g, const HM& h,
-                        const double* l, const double* u, double delta, double* s) {
+                        const double* l, const double* u, double delta, double* s,
+                        double* qs, bool* qs_ok) {
+    *qs_ok = false;
     const double gnorm = vnorm2<N, kOol>(g);
     if (gnorm == 0.0) {
 #pragma unroll
@@ -218,9 +220,16 @@ GA_FN void cauchy_point(const double* x, const double* g, const HM& h,
 #pragma unroll
         for (int i = 0; i < N; ++i) out[i] = sclamp(x[i] - alpha * g[i], l[i], u[i]) - x[i];
     };
+    // q(t) of the current trial when the radius test let ok() compute it:
+    // tron_step's qc = q(s) (tron.cpp:278) reuses it (same inputs, same bits)
+    double mt = 0.0;
+    bool mt_ok = false;
     auto ok = [&](const double* st) {
+        mt_ok = false;
         if (!(vnorm2<N, kOol>(st) <= delta)) return false;
-        return model<N>(g, h, st) <= kTronMu0 * vdot<N>(g, st);
+        mt = model<N>(g, h, st);
+        mt_ok = true;
+        return mt <= kTronMu0 * vdot<N>(g, st);
     };
     // One trial site (instruction-cache footprint: this is the hottest loop of
     // the lane phase, ~21 trials per step): phase 0 is alpha0, phase 1 the
@@ -240,6 +249,8 @@ GA_FN void cauchy_point(const double* x, const double* g, const HM& h,
         }
 #pragma unroll
         for (int i = 0; i < N; ++i) s[i] = t[i];
+        *qs = mt;
+        *qs_ok = mt_ok;
         if (phase == 2 && o && cnt > 0) return;
         if (phase == 1) {
             if (cnt >= 20) return;
@@ -429,25 +440,30 @@ struct SerialSearch {
     GA_FN void hessian(const P& prob, const double* x, double* h) const { prob.hessian(x, h); }
     template <int N, class HM>
     GA_FN void cauchy(const double* x, const double* g, const HM& h, const double* l,
-                      const double* u, double delta, double* s) const {
-        cauchy_point<N, kOolDivSqrt>(x, g, h, l, u, delta, s);
+                      const double* u, double delta, double* s, double* qs, bool* qs_ok) const {
+        cauchy_point<N, kOolDivSqrt>(x, g, h, l, u, delta, s, qs, qs_ok);
     }
-    // Projected line search on s + beta d (tron.cpp:279-291); returns the step.
+    // Projected line search on s + beta d (tron.cpp:279-291); returns the step
+    // and its model value q(stp) (tron.cpp:292): the accepted trial's, or,
+    // when no trial is accepted (stp = s), qc = q(s) — the same bits the
+    // reference's separate model() call produces.
     template <int N, class HM>
-    GA_FN void line_search(const double* x, const double* g, const HM& h, const double* l,
-                           const double* u, const double* s, const double* d, double qc,
-                           double* stp) const {
+    GA_FN double line_search(const double* x, const double* g, const HM& h, const double* l,
+                             const double* u, const double* s, const double* d, double qc,
+                             double* stp) const {
         double beta = 1.0;
         GA_STAT(0);
         for (int ls = 0; ls < 20; ++ls) {
             GA_STAT(4);
 #pragma unroll
             for (int i = 0; i < N; ++i) stp[i] = sclamp(x[i] + s[i] + beta * d[i], l[i], u[i]) - x[i];
-            if (model<N>(g, h, stp) <= qc) return;
+            const double q = model<N>(g, h, stp);
+            if (q <= qc) return q;
             beta *= 0.5;
         }
 #pragma unroll
         for (int i = 0; i < N; ++i) stp[i] = s[i];
+        return qc;
     }
 };
 
@@ -501,7 +517,9 @@ struct TileSearch {
 
     template <int N, class HM>
     __device__ void cauchy(const double* x, const double* g, const HM& h, const double* l,
-                           const double* u, double delta, double* s) const {
+                           const double* u, double delta, double* s, double* qs,
+                           bool* qs_ok) const {
+        *qs_ok = false;
         const double gnorm = vnorm2<N>(g);
         if (gnorm == 0.0) {
 #pragma unroll
@@ -523,14 +541,19 @@ struct TileSearch {
             else if (dir > 0) c = 2 + (round - 1) * T + rank;
             else c = -((T - 1) + (round - 1) * T + rank);
             const bool valid = dir > 0 ? c <= 20 : c >= -40;
-            bool okc = false;
+            bool okc = false, mok = false;
+            double mv = 0.0;
             if (valid) {
                 double a = alpha0;
                 for (int k = 0; k < c; ++k) a *= 2.0;
                 for (int k = 0; k < -c; ++k) a *= 0.5;
 #pragma unroll
                 for (int i = 0; i < N; ++i) mys[i] = sclamp(x[i] - a * g[i], l[i], u[i]) - x[i];
-                okc = vnorm2<N>(mys) <= delta && model<N>(g, h, mys) <= kTronMu0 * vdot<N>(g, mys);
+                if (vnorm2<N>(mys) <= delta) {
+                    mv = model<N>(g, h, mys);
+                    mok = true;
+                    okc = mv <= kTronMu0 * vdot<N>(g, mys);
+                }
             }
             const unsigned okm = ballot(okc);
             int src = -1;      // lane whose trial step becomes s
@@ -556,15 +579,19 @@ struct TileSearch {
                 else if (kb + T - 1 >= 40) src = 40 - kb;  // none up to 2^-40: last trial's step
                 else done = false;
             }
-            if (src >= 0) bcast<N>(mys, src, s);
+            if (src >= 0) {
+                bcast<N>(mys, src, s);
+                *qs = __shfl_sync(mask, mv, src, T);
+                *qs_ok = __shfl_sync(mask, mok ? 1 : 0, src, T) != 0;
+            }
             if (done) return;
         }
     }
 
     template <int N, class HM>
-    __device__ void line_search(const double* x, const double* g, const HM& h, const double* l,
-                                const double* u, const double* s, const double* d, double qc,
-                                double* stp) const {
+    __device__ double line_search(const double* x, const double* g, const HM& h, const double* l,
+                                  const double* u, const double* s, const double* d, double qc,
+                                  double* stp) const {
         double myst[N];
         for (int tb = 0; tb < 20; tb += T) {
             const int t = tb + rank;
@@ -572,12 +599,18 @@ struct TileSearch {
             for (int k = 0; k < t; ++k) beta *= 0.5;
 #pragma unroll
             for (int i = 0; i < N; ++i) myst[i] = sclamp(x[i] + s[i] + beta * d[i], l[i], u[i]) - x[i];
-            const bool okt = (t < 20) ? (model<N>(g, h, myst) <= qc) : false;
+            const double q = model<N>(g, h, myst);
+            const bool okt = (t < 20) ? (q <= qc) : false;
             const unsigned okm = ballot(okt);
-            if (okm) { bcast<N>(myst, __ffs(okm) - 1, stp); return; }
+            if (okm) {
+                const int src = __ffs(okm) - 1;
+                bcast<N>(myst, src, stp);
+                return __shfl_sync(mask, q, src, T);
+            }
         }
 #pragma unroll
         for (int i = 0; i < N; ++i) stp[i] = s[i];
+        return qc;
     }
 };
 #endif
@@ -632,15 +665,16 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
 
     double s[N], d[N];
     GA_CLK(1);
-    search.template cauchy<N>(st.x, g, h, l, u, st.delta, s);
+    double qs = 0.0;
+    bool qs_ok = false;
+    search.template cauchy<N>(st.x, g, h, l, u, st.delta, s, &qs, &qs_ok);
     GA_CLK(2);
     subspace_cg<N, Search::kOolDivSqrt>(st.x, g, h, l, u, st.delta, cfg, s, d);
     GA_CLK(3);
 
-    const double qc = model<N>(g, h, s);
+    const double qc = qs_ok ? qs : model<N>(g, h, s);
     double stp[N];
-    search.template line_search<N>(st.x, g, h, l, u, s, d, qc, stp);
-    const double q = model<N>(g, h, stp);
+    const double q = search.template line_search<N>(st.x, g, h, l, u, s, d, qc, stp);
     double xt[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) xt[i] = sclamp(st.x[i] + stp[i], l[i], u[i]);

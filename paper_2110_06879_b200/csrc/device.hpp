@@ -118,10 +118,6 @@ void launch_buses(const DevNet& n, const DevState& s, DevScalars* sc, cudaStream
 // Bus QP fused with z, y and all four residual norms (the iteration path).
 void launch_bus_zy(const DevNet& n, const DevState& s, double beta, DevScalars* sc,
                    cudaStream_t st);
-void launch_buses_warp(const DevNet& n, const DevState& s, DevScalars* sc, cudaStream_t st);
-// z update + y update + residual/z norms, fused (one pass over m).
-void launch_zy(const DevNet& n, const DevState& s, double beta, DevScalars* sc,
-               cudaStream_t st);
 // Separate z / y phases (phase-replay API).
 void launch_z_only(const DevNet& n, const DevState& s, double beta, cudaStream_t st);
 void launch_y_only(const DevNet& n, const DevState& s, cudaStream_t st);

@@ -70,12 +70,12 @@ __global__ void __launch_bounds__(kBlock) gen_kernel(DevNet n, DevState s) {
 }
 
 // ---- buses (kernels.cpp:294-413) ----------------------------------------
-// One thread per bus.  Variables: [0] w, [1] theta, then one duplicate per
-// row in gen_p, gen_q, flow_p, flow_q order.  A's entries are implied by the
-// group of each column.  Sums run over columns in the reference's order;
-// columns whose A entry is an exact zero are skipped when every c is finite
-// (the skipped term is a signed zero added to an accumulator that started
-// at +0.0 — exact), otherwise the dense loop is used.
+// Per bus, variables: [0] w, [1] theta, then one duplicate per row in gen_p,
+// gen_q, flow_p, flow_q order.  A's entries are implied by the group of each
+// column.  Sums run over columns in the reference's order; columns whose A
+// entry is an exact zero are skipped when every c is finite (the skipped
+// term is a signed zero added to an accumulator that started at +0.0 —
+// exact), otherwise the dense loop is used.
 __device__ __forceinline__ double a_coef(int r, int grp, double gs, double bs, bool ref) {
     // grp: 0 = w, 1 = theta, 2 = gen_p, 3 = gen_q, 4 = flow_p, 5 = flow_q
     switch (r) {
@@ -84,190 +84,6 @@ __device__ __forceinline__ double a_coef(int r, int grp, double gs, double bs, b
         default: return (ref && grp == 1) ? 1.0 : 0.0;
     }
 }
-
-__global__ void __launch_bounds__(kBlock) bus_kernel(DevNet n, DevState s, DevScalars* sc) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    double dual = 0.0;
-    if (i < n.nb) {
-        const int* grp = n.bus_grp + 7 * i;
-        const int* rows = n.bus_rows;
-        const bool ref = i == n.ref_bus;
-        const double gs = n.b_gs[i], bs = n.b_bs[i];
-        auto cval = [&](int row) { return s.rho[row] * (s.x[row] + s.z[row]) + s.y[row]; };
-
-        double q0 = 0.0, c0 = 0.0, q1 = 0.0, c1 = 0.0;
-        for (int k = grp[0]; k < grp[1]; ++k) {
-            const int row = rows[k];
-            q0 += s.rho[row];
-            c0 += cval(row);
-        }
-        for (int k = grp[1]; k < grp[2]; ++k) {
-            const int row = rows[k];
-            q1 += s.rho[row];
-            c1 += cval(row);
-        }
-        if (q0 == 0.0) q0 = 1.0;
-        if (q1 == 0.0) q1 = 1.0;
-        const int nc = ref ? 3 : 2;
-
-        // finiteness of every c decides the sparse (exact) vs dense path
-        bool finite = sfinite(c0) && sfinite(c1);
-        for (int k = grp[2]; k < grp[6] && finite; ++k) finite = sfinite(cval(rows[k]));
-
-        double S[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, rhs[3] = {0, 0, 0};
-        const double bvec[3] = {n.b_pd[i], n.b_qd[i], 0.0};
-        if (finite) {
-            const double a00 = -gs, a10 = bs;
-            double s00 = 0.0, s01 = 0.0, s11 = 0.0, s22 = 0.0, r0 = 0.0, r1 = 0.0, r2 = 0.0;
-            // column 0 (w)
-            s00 += a00 * a00 / q0;
-            s01 += a00 * a10 / q0;
-            s11 += a10 * a10 / q0;
-            r0 += a00 * c0 / q0;
-            r1 += a10 * c0 / q0;
-            // column 1 (theta): only the REF row is non-zero
-            if (ref) {
-                s22 += 1.0 * 1.0 / q1;
-                r2 += 1.0 * c1 / q1;
-            }
-            // S[0][0] / rhs[0]: gen_p then flow_p columns (+1 / -1)
-            for (int k = grp[2]; k < grp[3]; ++k) {
-                const int row = rows[k];
-                const double q = s.rho[row];
-                s00 += 1.0 * 1.0 / q;
-                r0 += 1.0 * cval(row) / q;
-            }
-            for (int k = grp[4]; k < grp[5]; ++k) {
-                const int row = rows[k];
-                const double q = s.rho[row];
-                s00 += -1.0 * -1.0 / q;
-                r0 += -1.0 * cval(row) / q;
-            }
-            // S[1][1] / rhs[1]: gen_q then flow_q columns
-            for (int k = grp[3]; k < grp[4]; ++k) {
-                const int row = rows[k];
-                const double q = s.rho[row];
-                s11 += 1.0 * 1.0 / q;
-                r1 += 1.0 * cval(row) / q;
-            }
-            for (int k = grp[5]; k < grp[6]; ++k) {
-                const int row = rows[k];
-                const double q = s.rho[row];
-                s11 += -1.0 * -1.0 / q;
-                r1 += -1.0 * cval(row) / q;
-            }
-            // S[1][0] = 0 + bs*(-gs)/q0: commutative product, same bits as s01
-            S[0] = s00; S[1] = s01; S[3] = s01; S[4] = s11;
-            S[8] = s22;
-            rhs[0] = r0 - bvec[0];
-            rhs[1] = r1 - bvec[1];
-            rhs[2] = r2 - bvec[2];
-        } else {
-            // dense reference loop (kernels.cpp:350-361), any column value
-            auto col = [&](int j, int* g, double* qj, double* cj) {
-                if (j == 0) { *g = 0; *qj = q0; *cj = c0; return; }
-                if (j == 1) { *g = 1; *qj = q1; *cj = c1; return; }
-                const int k = grp[2] + (j - 2);
-                int gg = 2;
-                while (k >= grp[gg + 1]) ++gg;
-                const int row = rows[k];
-                *g = gg;
-                *qj = s.rho[row];
-                *cj = cval(row);
-            };
-            const int nv = 2 + (grp[6] - grp[2]);
-            for (int r = 0; r < nc; ++r) {
-                for (int t = 0; t < nc; ++t) {
-                    double acc = 0.0;
-                    for (int j = 0; j < nv; ++j) {
-                        int g; double qj, cj;
-                        col(j, &g, &qj, &cj);
-                        acc += a_coef(r, g, gs, bs, ref) * a_coef(t, g, gs, bs, ref) / qj;
-                    }
-                    S[r * 3 + t] = acc;
-                }
-                double acc = 0.0;
-                for (int j = 0; j < nv; ++j) {
-                    int g; double qj, cj;
-                    col(j, &g, &qj, &cj);
-                    acc += a_coef(r, g, gs, bs, ref) * cj / qj;
-                }
-                rhs[r] = acc - bvec[r];
-            }
-        }
-
-        // Gaussian elimination with partial pivoting (kernels.cpp:364-391)
-        double mu[3] = {0, 0, 0};
-        bool singular = false;
-        {
-            int piv[3] = {0, 1, 2};
-            for (int col = 0; col < nc && !singular; ++col) {
-                int best = col;
-                for (int r = col + 1; r < nc; ++r)
-                    if (fabs(S[piv[r] * 3 + col]) > fabs(S[piv[best] * 3 + col])) best = r;
-                const int tmp = piv[col]; piv[col] = piv[best]; piv[best] = tmp;
-                const double d = S[piv[col] * 3 + col];
-                if (fabs(d) < 1e-14) { singular = true; break; }
-                for (int r = col + 1; r < nc; ++r) {
-                    const double f = S[piv[r] * 3 + col] / d;
-                    for (int s2 = col; s2 < nc; ++s2) S[piv[r] * 3 + s2] -= f * S[piv[col] * 3 + s2];
-                    rhs[piv[r]] -= f * rhs[piv[col]];
-                }
-            }
-            if (!singular) {
-                for (int col = nc - 1; col >= 0; --col) {
-                    double acc = rhs[piv[col]];
-                    for (int s2 = col + 1; s2 < nc; ++s2) acc -= S[piv[col] * 3 + s2] * mu[s2];
-                    mu[col] = acc / S[piv[col] * 3 + col];
-                }
-            }
-        }
-        if (singular) {
-            atomicMin(&sc->singular_bus, i);
-        } else {
-            // xbar = Q^-1 (c - A' mu) (kernels.cpp:394-399), dense in r
-            auto solve_col = [&](int g, double cj, double qj) {
-                double acc = cj;
-                for (int r = 0; r < nc; ++r) acc -= a_coef(r, g, gs, bs, ref) * mu[r];
-                return acc / qj;
-            };
-            const double w = solve_col(0, c0, q0);
-            const double th = solve_col(1, c1, q1);
-            s.bus_w[i] = w;
-            s.bus_theta[i] = th;
-            for (int k = grp[0]; k < grp[1]; ++k) {
-                const int row = rows[k];
-                dual = smax(dual, abs_or_zero(w - s.xbar[row]));
-                s.xbar[row] = w;
-            }
-            for (int k = grp[1]; k < grp[2]; ++k) {
-                const int row = rows[k];
-                dual = smax(dual, abs_or_zero(th - s.xbar[row]));
-                s.xbar[row] = th;
-            }
-            for (int gg = 2; gg < 6; ++gg)
-                for (int k = grp[gg]; k < grp[gg + 1]; ++k) {
-                    const int row = rows[k];
-                    const double v = solve_col(gg, cval(row), s.rho[row]);
-                    dual = smax(dual, abs_or_zero(v - s.xbar[row]));
-                    s.xbar[row] = v;
-                }
-        }
-    }
-    double vals[1] = {dual};
-    unsigned long long* const dst[1] = {&sc->dual_inf};
-    block_max_atomic<1>(vals, dst);
-}
-
-// Warp-per-bus variant (the one launched).  The thread-per-bus kernel above
-// walks each bus's CSR rows four times as chains of dependent gathers and is
-// latency-bound with a long tail on high-degree buses; here the 32 lanes of
-// a warp gather the bus's rows in parallel into shared memory once (rho,
-// c = rho(x+z)+y, old xbar), lane 0 runs the ordered sums and the 3x3
-// elimination exactly as above, and the lanes write the rows back in
-// parallel.  Same arithmetic, same order, same bits.
-constexpr int kBusWarps = 8;
-constexpr int kBusCap = 96;  // staged rows per bus; larger buses read the rest from global
 
 // Gaussian elimination with partial pivoting on the NC x NC system
 // (kernels.cpp:364-391) with register-resident rows: the reference permutes
@@ -322,189 +138,11 @@ __device__ __forceinline__ bool ge_solve(double* S, double* rhs, double* mu) {
     return true;
 }
 
-__global__ void __launch_bounds__(kBusWarps * 32) bus_warp_kernel(DevNet n, DevState s,
-                                                                  DevScalars* sc) {
-    __shared__ double sq[kBusWarps][kBusCap], scv[kBusWarps][kBusCap], sxb[kBusWarps][kBusCap];
-    __shared__ double sts[kBusWarps][kBusCap], str[kBusWarps][kBusCap];  // S / rhs terms of dup rows
-    __shared__ double sres[kBusWarps][6];  // mu0..2, w, theta, singular flag
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    double dual = 0.0;
-    const int nbus = n.buses_count();
-    for (int t = blockIdx.x * kBusWarps + wib; t < nbus; t += gridDim.x * kBusWarps) {
-        const int i = n.bus_at(t);
-        const int* grp = n.bus_grp + 7 * i;
-        int g[7];
-#pragma unroll
-        for (int k = 0; k < 7; ++k) g[k] = grp[k];
-        const int cnt = g[6] - g[0];
-        const int* rows = n.bus_rows + g[0];
-        for (int k = lane; k < cnt && k < kBusCap; k += 32) {
-            const int row = rows[k];
-            const double q = s.rho[row];
-            const double c = q * (s.x[row] + s.z[row]) + s.y[row];
-            sq[wib][k] = q;
-            scv[wib][k] = c;
-            sxb[wib][k] = s.xbar[row];
-            // the per-column terms of the S / rhs sums (kernels.cpp:350-361)
-            // are independent of each other: form them in parallel here and
-            // leave only the ordered additions to lane 0
-            if (k >= g[2] - g[0]) {
-                const bool plus = k < g[4] - g[0];  // gen_p / gen_q columns carry +1, flows -1
-                const double a = plus ? 1.0 : -1.0;
-                sts[wib][k] = a * a / q;
-                str[wib][k] = a * c / q;
-            }
-        }
-        __syncwarp();
-        const bool ref = i == n.ref_bus;
-        const int nc = ref ? 3 : 2;
-        const double gs = n.b_gs[i], bs = n.b_bs[i];
-        auto cq = [&](int k, double* c, double* q) {  // local row k -> (c, rho)
-            if (k < kBusCap) { *c = scv[wib][k]; *q = sq[wib][k]; return; }
-            const int row = rows[k];
-            *q = s.rho[row];
-            *c = *q * (s.x[row] + s.z[row]) + s.y[row];
-        };
-        if (lane == 0) {
-            double q0 = 0.0, c0 = 0.0, q1 = 0.0, c1 = 0.0, c, q;
-            for (int k = 0; k < g[1] - g[0]; ++k) { cq(k, &c, &q); q0 += q; c0 += c; }
-            for (int k = g[1] - g[0]; k < g[2] - g[0]; ++k) { cq(k, &c, &q); q1 += q; c1 += c; }
-            if (q0 == 0.0) q0 = 1.0;
-            if (q1 == 0.0) q1 = 1.0;
-            bool finite = sfinite(c0) && sfinite(c1);
-            for (int k = g[2] - g[0]; k < cnt && finite; ++k) { cq(k, &c, &q); finite = sfinite(c); }
-            double S[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, rhs[3] = {0, 0, 0};
-            const double bvec[3] = {n.b_pd[i], n.b_qd[i], 0.0};
-            if (finite) {
-                const double a00 = -gs, a10 = bs;
-                double s00 = 0.0, s01 = 0.0, s11 = 0.0, s22 = 0.0, r0 = 0.0, r1 = 0.0, r2 = 0.0;
-                s00 += a00 * a00 / q0;
-                s01 += a00 * a10 / q0;
-                s11 += a10 * a10 / q0;
-                r0 += a00 * c0 / q0;
-                r1 += a10 * c0 / q0;
-                if (ref) {
-                    s22 += 1.0 * 1.0 / q1;
-                    r2 += 1.0 * c1 / q1;
-                }
-                // staged terms (same expressions as below, formed in parallel)
-                auto term = [&](int k, double a, double* ts, double* tr) {
-                    if (k < kBusCap) { *ts = sts[wib][k]; *tr = str[wib][k]; return; }
-                    cq(k, &c, &q);
-                    *ts = a * a / q;
-                    *tr = a * c / q;
-                };
-                double ts, tr;
-                for (int k = g[2] - g[0]; k < g[3] - g[0]; ++k) {  // gen_p (+1)
-                    term(k, 1.0, &ts, &tr);
-                    s00 += ts;
-                    r0 += tr;
-                }
-                for (int k = g[4] - g[0]; k < g[5] - g[0]; ++k) {  // flow_p (-1)
-                    term(k, -1.0, &ts, &tr);
-                    s00 += ts;
-                    r0 += tr;
-                }
-                for (int k = g[3] - g[0]; k < g[4] - g[0]; ++k) {  // gen_q (+1)
-                    term(k, 1.0, &ts, &tr);
-                    s11 += ts;
-                    r1 += tr;
-                }
-                for (int k = g[5] - g[0]; k < g[6] - g[0]; ++k) {  // flow_q (-1)
-                    term(k, -1.0, &ts, &tr);
-                    s11 += ts;
-                    r1 += tr;
-                }
-                S[0] = s00; S[1] = s01; S[3] = s01; S[4] = s11;
-                S[8] = s22;
-                rhs[0] = r0 - bvec[0];
-                rhs[1] = r1 - bvec[1];
-                rhs[2] = r2 - bvec[2];
-            } else {
-                // dense reference loop (kernels.cpp:350-361)
-                auto col = [&](int j, int* gg, double* qj, double* cj) {
-                    if (j == 0) { *gg = 0; *qj = q0; *cj = c0; return; }
-                    if (j == 1) { *gg = 1; *qj = q1; *cj = c1; return; }
-                    const int k = g[2] - g[0] + (j - 2);
-                    int grp_id = 2;
-                    while (k >= g[grp_id + 1] - g[0]) ++grp_id;
-                    *gg = grp_id;
-                    cq(k, cj, qj);
-                };
-                const int nv = 2 + (g[6] - g[2]);
-                for (int r = 0; r < nc; ++r) {
-                    for (int t = 0; t < nc; ++t) {
-                        double acc = 0.0;
-                        for (int j = 0; j < nv; ++j) {
-                            int gg; double qj, cj;
-                            col(j, &gg, &qj, &cj);
-                            acc += a_coef(r, gg, gs, bs, ref) * a_coef(t, gg, gs, bs, ref) / qj;
-                        }
-                        S[r * 3 + t] = acc;
-                    }
-                    double acc = 0.0;
-                    for (int j = 0; j < nv; ++j) {
-                        int gg; double qj, cj;
-                        col(j, &gg, &qj, &cj);
-                        acc += a_coef(r, gg, gs, bs, ref) * cj / qj;
-                    }
-                    rhs[r] = acc - bvec[r];
-                }
-            }
-            double mu[3] = {0, 0, 0};
-            const bool singular = ref ? !ge_solve<3>(S, rhs, mu) : !ge_solve<2>(S, rhs, mu);
-            if (!singular) {
-                double acc = c0;
-                for (int r = 0; r < nc; ++r) acc -= a_coef(r, 0, gs, bs, ref) * mu[r];
-                sres[wib][3] = acc / q0;
-                acc = c1;
-                for (int r = 0; r < nc; ++r) acc -= a_coef(r, 1, gs, bs, ref) * mu[r];
-                sres[wib][4] = acc / q1;
-                s.bus_w[i] = sres[wib][3];
-                s.bus_theta[i] = sres[wib][4];
-            } else {
-                atomicMin(&sc->singular_bus, i);
-            }
-            sres[wib][0] = mu[0];
-            sres[wib][1] = mu[1];
-            sres[wib][2] = mu[2];
-            sres[wib][5] = singular ? 1.0 : 0.0;
-        }
-        __syncwarp();
-        if (sres[wib][5] == 0.0) {
-            const double mu[3] = {sres[wib][0], sres[wib][1], sres[wib][2]};
-            const double w = sres[wib][3], th = sres[wib][4];
-            for (int k = lane; k < cnt; k += 32) {
-                const int row = rows[k];
-                double v;
-                if (k < g[1] - g[0]) v = w;
-                else if (k < g[2] - g[0]) v = th;
-                else {
-                    int gg = 2;
-                    while (k >= g[gg + 1] - g[0]) ++gg;
-                    double c, q;
-                    cq(k, &c, &q);
-                    double acc = c;
-                    for (int r = 0; r < nc; ++r) acc -= a_coef(r, gg, gs, bs, ref) * mu[r];
-                    v = acc / q;
-                }
-                const double old = k < kBusCap ? sxb[wib][k] : s.xbar[row];
-                dual = smax(dual, abs_or_zero(v - old));
-                s.xbar[row] = v;
-            }
-        }
-        __syncwarp();
-    }
-    double vals[1] = {dual};
-    unsigned long long* const dst[1] = {&sc->dual_inf};
-    block_max_atomic<1>(vals, dst);
-}
-
 // Block-staged bus kernel (the one launched), optionally fused with the z / y
 // updates and all four residual norms.
 //
-// The warp-per-bus kernel above spends its time issuing lane 0's serial code
-// (ncu: 4 active threads per warp, 59% issue-slot busy).  Here a block of
+// A warp-per-bus formulation (previous version) spent its time issuing lane
+// 0's serial code (ncu: 4 active threads per warp, 59% issue-slot busy).  Here a block of
 // kBB threads owns kBB consecutive buses and works in three phases:
 //   1. gather: the block's rows (CSR, contiguous per bus) are spread over all
 //      threads; each thread loads rho, x, z, y of a row and stages either
@@ -836,29 +474,6 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
     }
 }
 
-// ---- fused z / y / residual (kernels.cpp:415-428, decomp.cpp:59-72) -----
-__global__ void __launch_bounds__(kBlock) zy_kernel(DevNet n, DevState s, double beta,
-                                                    DevScalars* sc) {
-    double pr = 0.0, zi = 0.0, zd = 0.0;
-    const int nrows = n.rows_count();
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nrows; t += gridDim.x * blockDim.x) {
-        const int k = n.row_at(t);
-        const double x = s.x[k], xb = s.xbar[k], rho = s.rho[k];
-        const double zold = s.z[k], y = s.y[k];
-        const double r = x - xb;
-        const double z = -(s.lambda[k] + y + rho * r) / (rho + beta);
-        const double res = x - xb + z;
-        s.z[k] = z;
-        s.y[k] = y + rho * res;
-        pr = smax(pr, abs_or_zero(res));
-        zi = smax(zi, abs_or_zero(z));
-        zd = smax(zd, abs_or_zero(z - zold));
-    }
-    double vals[3] = {pr, zi, zd};
-    unsigned long long* const dst[3] = {&sc->primal_inf, &sc->z_inf, &sc->z_drift};
-    block_max_atomic<3>(vals, dst);
-}
-
 __global__ void z_only_kernel(DevNet n, DevState s, double beta) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n.rows_count()) return;
@@ -966,18 +581,7 @@ void measure_fp64_peak(double* tflops_mul_add, double* tflops_fma) {
     cudaFree(out);
 }
 
-namespace {
-int sm_count() {
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
-}
-}  // namespace
+
 
 void launch_generators(const DevNet& n, const DevState& s, cudaStream_t st) {
     const int c = n.gens_count();
@@ -993,35 +597,6 @@ void launch_bus_zy(const DevNet& n, const DevState& s, double beta, DevScalars* 
                    cudaStream_t st) {
     const int c = n.buses_count();
     if (c > 0) bus_block_kernel<true><<<(c + kBB - 1) / kBB, kBB, 0, st>>>(n, s, beta, sc);
-}
-
-// Warp-per-bus kernel (previous version, kept for A/B timing).
-void launch_buses_warp(const DevNet& n, const DevState& s, DevScalars* sc, cudaStream_t st) {
-    const int c = n.buses_count();
-    if (c <= 0) return;
-    static int max_blocks = 0;
-    if (max_blocks == 0) {
-        int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bus_warp_kernel, kBusWarps * 32, 0);
-        max_blocks = sm_count() * (per_sm > 0 ? per_sm : 1);
-    }
-    int blocks = (c + kBusWarps - 1) / kBusWarps;
-    if (blocks > max_blocks) blocks = max_blocks;
-    bus_warp_kernel<<<blocks, kBusWarps * 32, 0, st>>>(n, s, sc);
-}
-
-// Reference-shaped one-thread-per-bus kernel (kept for A/B timing; whole net).
-void launch_buses_thread(const DevNet& n, const DevState& s, DevScalars* sc, cudaStream_t st) {
-    if (n.nb > 0) bus_kernel<<<blocks_for(n.nb), kBlock, 0, st>>>(n, s, sc);
-}
-
-void launch_zy(const DevNet& n, const DevState& s, double beta, DevScalars* sc,
-               cudaStream_t st) {
-    const int c = n.rows_count();
-    if (c <= 0) return;
-    int blocks = blocks_for(c);
-    if (blocks > sm_count() * 8) blocks = sm_count() * 8;
-    zy_kernel<<<blocks, kBlock, 0, st>>>(n, s, beta, sc);
 }
 
 void launch_z_only(const DevNet& n, const DevState& s, double beta, cudaStream_t st) {

@@ -679,16 +679,22 @@ void launch_branches(const DevNet& n, const DevState& s, const BranchCfg& cfg, D
     if (n.nl <= 0) return;
     const Work w = work_of(n, s);
     cudaMemsetAsync(w.ctr, 0, kCounters * sizeof(int), st);
-    static int lane_blocks = 0, tile_blocks = 0, solo_blocks = 0;
     const size_t lane_smem =
         static_cast<size_t>(GA_LANE_HESS_SMEM ? kFieldsHess : kFields) * kLaneBlock * sizeof(double);
-    if (lane_blocks == 0) {
-        lane_blocks = persistent_blocks(lane_kernel, kLaneBlock, lane_smem);
-        tile_blocks = persistent_blocks(tile_kernel, kTileBlock, 0);
+    // persistent grid sizes (thread-safe one-time init; the pool's GPUs are identical)
+    struct Grids {
+        int lane, tile, solo;
+    };
+    static const Grids grids = [lane_smem] {
+        Grids gr;
+        gr.lane = persistent_blocks(lane_kernel, kLaneBlock, lane_smem);
+        gr.tile = persistent_blocks(tile_kernel, kTileBlock, 0);
         int dev = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&solo_blocks, cudaDevAttrMultiProcessorCount, dev);
-    }
+        cudaDeviceGetAttribute(&gr.solo, cudaDevAttrMultiProcessorCount, dev);
+        return gr;
+    }();
+    const int lane_blocks = grids.lane, tile_blocks = grids.tile, solo_blocks = grids.solo;
     const int total = n.n_lim + n.n_unl;
     const int need = (total + kLaneBlock - 1) / kLaneBlock;
     BranchCfg lc = cfg;

@@ -27,6 +27,7 @@
 // sequence of floating-point operations wherever and in whichever phase it
 // runs (the migration saves/restores exact state), so parity is bit-exact.
 #include <climits>
+#include <cstdlib>
 
 #include "branch_problem.cuh"
 #include "device.hpp"
@@ -698,7 +699,11 @@ void launch_branches(const DevNet& n, const DevState& s, const BranchCfg& cfg, D
     const int total = n.n_lim + n.n_unl;
     const int need = (total + kLaneBlock - 1) / kLaneBlock;
     BranchCfg lc = cfg;
-    lc.tile_slots = tile_blocks * (kTileBlock / kTile) / 2;  // per queue (two queues share)
+    static const int slot_mult = [] {  // scheduling knob (sweeps): switch point scale
+        const char* e = std::getenv("GRIDADMM_SLOT_MULT");
+        return e && std::atoi(e) > 0 ? std::atoi(e) : 1;
+    }();
+    lc.tile_slots = slot_mult * tile_blocks * (kTileBlock / kTile) / 2;  // per queue (two share)
     lane_kernel<<<lane_blocks < need ? lane_blocks : need, kLaneBlock, lane_smem, st>>>(n, s, lc,
                                                                                        w, sc);
     if (mid) cudaEventRecord(mid, st);

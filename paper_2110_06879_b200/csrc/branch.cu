@@ -699,9 +699,12 @@ void launch_branches(const DevNet& n, const DevState& s, const BranchCfg& cfg, D
     const int total = n.n_lim + n.n_unl;
     const int need = (total + kLaneBlock - 1) / kLaneBlock;
     BranchCfg lc = cfg;
-    static const int slot_mult = [] {  // scheduling knob (sweeps): switch point scale
+    // the lane phase keeps branches (throughput mode) while the active set
+    // exceeds twice the tile slots (swept 1/2/4: 2 best on both the bench
+    // window and a truncated full solve; GRIDADMM_SLOT_MULT overrides)
+    static const int slot_mult = [] {
         const char* e = std::getenv("GRIDADMM_SLOT_MULT");
-        return e && std::atoi(e) > 0 ? std::atoi(e) : 1;
+        return e && std::atoi(e) > 0 ? std::atoi(e) : 2;
     }();
     lc.tile_slots = slot_mult * tile_blocks * (kTileBlock / kTile) / 2;  // per queue (two share)
     lane_kernel<<<lane_blocks < need ? lane_blocks : need, kLaneBlock, lane_smem, st>>>(n, s, lc,

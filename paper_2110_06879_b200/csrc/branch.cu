@@ -6,22 +6,27 @@
 // the reference schedules it as a static block partition over std::threads
 // (proj/src/parallel.hpp:13-33).
 //
-// B200 schedule.  TRON cost per branch is heavy-tailed: at ACTIVSg70k scale
-// the median branch needs 2 iterations while ~5% run to the 200 cap, and
-// those ~4.5k capped solves are ~85% of all iterations — far too few to fill
-// 148 SMs one lane each.  So the phase runs in two kernels:
+// B200 schedule.  TRON cost per branch is heavy-tailed and changes over a
+// solve: early, ~255k trust-region steps per sweep with ~5k branches past 4
+// steps (the longest ~20); late, the same bulk plus a handful of rate-limited
+// branches whose AL loop runs all 10 rounds (~1,000 steps in one chain).  So
+// the phase runs in three kernels:
 //
 //  A. lane phase — a persistent grid where each lane owns one branch and
 //     advances it one trust-region iteration per loop trip, refilling from the
 //     work queue (warp-aggregated atomic) the moment its branch finishes.  A
-//     branch may take at most `lane_budget` iterations here; if it is not done
-//     its resumable state (TRON iterate, radius, iteration, AL round) is saved
-//     and it is pushed to an overflow queue.
-//  B. tile phase — the overflow branches (the heavy tail) are resumed by tiles
-//     of 8 lanes.  All lanes of a tile hold the replicated iterate; the Cauchy
-//     search and the projected line search (the loops with many trials) are
-//     evaluated 8 trials at a time (TileSearch in tron.cuh), so a capped
-//     branch runs several times faster and 8x more lanes work on the tail.
+//     branch stays up to `lane_cap` steps while more branches are active than
+//     twice the tile slots (throughput mode), up to `lane_budget` after; then
+//     its resumable state (TRON iterate, radius, iteration, AL round) is
+//     saved and it is pushed to an overflow queue.
+//  B. tile phase — the overflow branches are resumed by tiles of 8 lanes (or
+//     whole warps when a queue is short).  All lanes of a tile hold the
+//     replicated iterate; the Cauchy search and the projected line search
+//     (the loops with many trials) are evaluated 8 (32) trials at a time
+//     (TileSearch in tron.cuh).  After `tile_budget` steps a branch is handed
+//     on again.
+//  C. solo phase — one warp per branch, one block per SM, for the few very
+//     long solves (their sequential chain bounds the late iterations).
 //
 // Results do not depend on the schedule: every branch executes the identical
 // sequence of floating-point operations wherever and in whichever phase it

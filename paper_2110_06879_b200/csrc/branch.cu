@@ -451,7 +451,8 @@ __global__ void __launch_bounds__(kTileBlock, GA_TILE_MINB) tile_kernel(DevNet n
 #ifndef GA_TILE_TAIL
 #define GA_TILE_TAIL 1
 #endif
-    const int half_warps = GA_TILE_TAIL ? (int)(gridDim.x * (kTileBlock / 32) / 2) : -1;
+    const int half_warps =
+        GA_TILE_TAIL ? (int)(gridDim.x * (kTileBlock / 32) * cfg.tail_num / 4) : -1;
     // 8-lane tiles hand branches that exceed cfg.tile_budget steps to the
     // solo phase (one warp per branch, one block per SM).
     auto run6 = [&] {

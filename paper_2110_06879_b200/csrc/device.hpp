@@ -104,6 +104,7 @@ struct BranchCfg {
     int lane_budget = 4;  // lane-phase steps of a branch once the active set fits the tiles
     int lane_cap = 16;    // lane-phase steps while the active set exceeds the tile slots (swept)
     int tile_slots = 0;   // set by the launcher: tiles available per queue
+    int tail_num = 2;     // whole-warp tiles when a queue <= tail_num/4 of the grid's warps
     int tile_budget = 48; // steps in the 8-lane tile phase before the solo phase takes over (0 = off)
 };
 

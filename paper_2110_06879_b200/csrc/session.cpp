@@ -365,6 +365,11 @@ BranchCfg branch_cfg(const SolverConfig& c) {
         return e ? std::atoi(e) : -1;
     }();
     if (tile_budget >= 0) b.tile_budget = tile_budget;
+    static const int tail_num = [] {
+        const char* e = std::getenv("GRIDADMM_TAIL_NUM");
+        return e ? std::atoi(e) : -1;
+    }();
+    if (tail_num >= 0) b.tail_num = tail_num;
     static const int lane_cap = [] {
         const char* e = std::getenv("GRIDADMM_LANE_CAP");
         return e ? std::atoi(e) : -1;

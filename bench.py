@@ -1,45 +1,58 @@
 #!/usr/bin/env python3
-"""bench.py — ADMM iterations/s of the B200-native gridadmm on an
-ACTIVSg70k-shaped grid (BASELINE.json metric, config[3]).
+"""bench.py — ADMM iterations/s and time-to-converge of the B200-native
+gridadmm on an ACTIVSg70k-shaped grid (BASELINE.json metric, configs[3]),
+with the reference C++ solver timed on the same host.
 
-A "step" is one inner ADMM iteration of the two-level ADMM (generator
-projection -> branch NLPs -> bus consensus -> z/y/residual norms, plus the
-host's read of the four residual norms that drive the loop control;
-proj/src/driver.cpp:155-186) over the whole grid.  The first W iterations
-from the cold start are the warm-up, the next K are timed.
+A "step" is one inner ADMM iteration of the two-level ADMM over the whole
+grid: generator projection -> branch NLPs -> bus consensus -> z / y /
+residual norms, plus the host's read of the norms that drive the loop
+control (proj/src/driver.cpp:155-186).  The first W iterations from the cold
+start are the warm-up, the next K are timed.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-* `value`: K x ranks / max-over-ranks device time of the K steps, state
-  resident in HBM, each step timed with CUDA events on the solver's stream
-  and an L2 flush (256 MiB write) between steps outside the events.
-* `e2e`: the same metric through the public C ABI with host buffers:
-  gridadmm_network_load'ed case -> gridadmm_solve (max_outer 1, max_inner
-  W+K; network + state upload, every iteration's norm readback and the
-  solution download inside the wall-clock region).
-* `roofline`: the branch-NLP kernel (dominant) against the measured FP64
-  DMUL+DADD peak (the kernel is built with -fmad=false for bit-exactness).
-* `cpu_baseline`: the reference C++ solver (oracle/_ref, compiled from the
-  reference sources with the pinned sincos) on this host's cores, timing a
-  bounded sample of the SAME iterations (its trajectory is bit-identical).
-* `converge`: time-to-converge of a full cold-start solve on the device
-  (penalty (100, 1e4), see CONVERGE_RHO) and a late-solve window (outer
-  iteration 10) timed on the device and with the reference CPU solver from
-  the same state (bit-identical residuals checked).
-* `--impl reference`: that reference solver alone (rank 0), same metric.
+Both arms run the same workload (WORKLOAD below, one shared `config` dict):
+the seeded synthetic ACTIVSg70k-shaped case (gridcases/synth.py: exactly the
+published 70,000 buses / 10,390 generators / 88,207 branches) with the
+reference's own preset for ACTIVSg70k (rho_pq 3e4, rho_va 3e5; capi.cpp:36)
+and its default tolerances (eps 1e-4, 20 x 1000 iterations).
 
-Multi-GPU (torchrun, N>1): the 70k-shaped grid is split over the N GPUs by
-the bus-graph partition, NCCL boundary exchange ("scaling": "strong");
-DESIGN.md §7.
+* `value`: K x ranks / max-over-ranks device time of the K steps, state
+  resident in HBM, each step timed with CUDA events on the solver's stream,
+  L2 flushed (256 MiB write) between steps outside the events.
+* `e2e`: the same iterations through the public C ABI with host buffers:
+  gridadmm_solve(max_outer 1, max_inner W+K) on a loaded network (network
+  upload, device cold start, every iteration's norm readback, solution
+  download inside the wall-clock region).
+* `converge`: time-to-converge of the full cold start through gridadmm_solve
+  (the reference's stop rules), with the reference's quality metrics (c_inf,
+  objective) of the result; `cpu_full_solve_s` is the reference's own full
+  solve of the same case on a box of this pool, measured once
+  (profiles/r02_converge_vs_reference_70k.json) because it runs ~30 minutes.
+* `track`: warm-start tracking, ACTIVSg25k-shaped, 30 snapshots
+  (BASELINE.json configs[4]), seconds per warm snapshot.
+* `roofline`: the branch-NLP kernels (dominant) against the measured FP64
+  DMUL+DADD peak (the kernels are built -fmad=false for bit-exactness); the
+  flop count is the lean op census of the C restatement on this workload.
+* `cpu_baseline`: the reference C++ solver (oracle/_ref, compiled unmodified
+  from the reference sources) through its own C ABI on all host cores,
+  timing a bounded sample of the SAME iterations (trajectory bit-identical).
+* `--impl reference`: that reference solver alone (rank 0), same metric,
+  same config; it imports only oracle/ and gridcases/, never the product.
+
+Multi-GPU (torchrun, N>1): the grid is split over the N GPUs by the
+bus-graph partition with NCCL boundary exchange (strong scaling).
 """
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
 import subprocess
 import sys
+import tempfile
 import threading
 import time
 
@@ -48,39 +61,46 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
+METRIC = "ADMM iters/sec & time-to-converge (s) on ACTIVSg70k; warm-start track s/step"
+DATA = "synthetic (gridcases.synth v2: seeded case30/case118 tiling to ACTIVSg70k dims)"
 L2_FLUSH_BYTES = 256 << 20
-SHAPE = "case_ACTIVSg70k"
-# Lean FP64 op census per TRON iteration (flops whose results are consumed,
-# branch evaluation + TRON core, amortized per-branch setup included),
-# measured with the C restatement's counters (oracle/gridadmm_oracle.c FL())
-# on the case2868rte-shaped synthetic grid, ACTIVSg70k preset, inner
-# iterations 1-20: 4-var 1588, 6-var 3329 flops/iteration.
-CENSUS_FLOPS = {4: 1588.0, 6: 3329.0}
-# Time-to-converge run: the synthetic ACTIVSg70k-shaped grid is not the real
-# case, and the paper's penalty pair for it (3e4 / 3e5) does not converge on
-# it in 20 x 1000 iterations; (100, 1e4) — the reference's own choice for its
-# bundled cases (proj/tests/acceptance.cpp:58-69) — converges (rho sweep,
-# scripts/rho_sweep.py).
-CONVERGE_RHO = (100.0, 1e4)
-LATE_OUTER = 10   # the late-window sample starts at this outer iteration
-LATE_STEPS = 5
+WORKLOAD = {"shape": "case_ACTIVSg70k", "seed": 2110, "preset": "case_ACTIVSg70k"}
+# Lean FP64 op census per reference TRON iteration (flops whose results are
+# consumed: branch evaluation + TRON core, amortized per-branch setup), from
+# the C restatement's counters (oracle/gridadmm_oracle.c FL()) on THIS
+# workload (profiles/r02_census_70k_window.json overrides these fallbacks).
+CENSUS_FLOPS = {4: 1529.5, 6: 3296.6}
+CENSUS_FILE = os.path.join(REPO, "profiles", "r02_census_70k_window.json")
+CPU_FULL_SOLVE_FILE = os.path.join(REPO, "profiles", "r02_converge_vs_reference_70k.json")
+TRACK_CPU_FILE = os.path.join(REPO, "profiles", "r02_track_25k_vs_reference.json")
+NCU_TRAFFIC_FILE = os.path.join(REPO, "profiles", "r02_ncu_traffic.jsonl")
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--shape", default=SHAPE)
-    ap.add_argument("--seed", type=int, default=2110)
-    ap.add_argument("--preset", default="case_ACTIVSg70k")
-    ap.add_argument("--cpu-steps", type=int, default=30, help="timed iterations of the CPU sample")
+    ap.add_argument("--cpu-steps", type=int, default=10, help="timed iterations of the CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-converge", action="store_true",
                     help="skip the time-to-converge run (full cold-start solve)")
+    ap.add_argument("--no-track", action="store_true", help="skip the warm-start tracking run")
     return ap.parse_args()
+
+
+def workload_config(args, dims):
+    """The `config` object both arms print (identical by construction)."""
+    nb, ng, nl = dims
+    w = WORKLOAD
+    return {"workload": f"{w['shape']}-shaped synthetic grid ({nb} buses, {ng} gens, {nl} "
+                        f"branches, m={2 * ng + 8 * nl}) cold start, preset {w['preset']}, "
+                        f"inner iterations {args.warmup}..{args.warmup + args.steps - 1}",
+            "shape": w["shape"], "seed": w["seed"], "preset": w["preset"],
+            "l2": "GPU arm: L2 flushed between timed steps by a 256 MiB write outside the "
+                  "timed events (state + network ~57 MB)"}
 
 
 class Dist:
@@ -115,13 +135,6 @@ class Dist:
             return v
         t = self.torch.tensor([v], dtype=self.torch.float64)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
-        return float(t.item())
-
-    def sum(self, v: float) -> float:
-        if self.world == 1:
-            return v
-        t = self.torch.tensor([v], dtype=self.torch.float64)
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
         return float(t.item())
 
     def close(self):
@@ -175,78 +188,103 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def case_file(shape: str, seed: int, d: Dist) -> str:
-    from paper_2110_06879_b200 import synth
+def case_file(d: Dist) -> str:
+    from gridcases import synth
     directory = os.path.join("/tmp", "gridadmm_cases")
-    path = os.path.join(directory, f"{shape}_synth_s{seed}.m")
+    path = synth.case_path(WORKLOAD["shape"], directory, seed=WORKLOAD["seed"])
     if d.rank == 0:
-        synth.ensure_case(shape, directory, seed=seed)
+        synth.ensure_case(WORKLOAD["shape"], directory, seed=WORKLOAD["seed"])
     d.barrier()
     while not os.path.exists(path):  # ranks on the same host share /tmp
         time.sleep(0.2)
     return path
 
 
-def cfg_kwargs(args, max_inner):
-    return dict(max_outer=1, max_inner=max_inner)
+def _load_json(path):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:  # noqa: BLE001
+        return None
 
 
-def reference_rate(path, args, iters_timed, workers):
-    """Reference C++ solver (oracle/_ref) on host cores: iterations/s over
-    iterations W..W+iters_timed-1 from the elapsed_s stamps of its own series
-    (proj/src/driver.cpp:190-191)."""
+# ---------------------------------------------------------------------------
+# reference arm: the unmodified reference solver through its own C ABI
+# ---------------------------------------------------------------------------
+
+def reference_run(path: str, warmup: int, steps: int, workers: int):
+    """gridadmm_solve of the reference library (oracle/_ref) with the preset
+    from its own table, max_outer 1, max_inner W+K, `workers` host threads;
+    iterations/s over iterations W..W+K-1 from the elapsed_s column of its
+    own convergence.csv (outputs.cpp:110-120).  Returns (rate, dt, wall,
+    series[n, 6], dims)."""
     import oracle
-    from paper_2110_06879_b200 import Config
     if not oracle.have_ref():
         raise RuntimeError("oracle/_ref/libgridadmm_ref.so missing")
-    c = Config(args.preset)
-    ref = oracle.RefNet(path)
-    n = args.warmup + iters_timed
+    h = oracle.ref_capi()
+    net = ctypes.c_void_p()
+    if h.gridadmm_network_load(os.fsencode(path), ctypes.byref(net)) != 0:
+        raise RuntimeError(h.gridadmm_last_error().decode())
+    dims = (h.gridadmm_network_num_buses(net), h.gridadmm_network_num_generators(net),
+            h.gridadmm_network_num_branches(net))
+    c = h.gridadmm_config_new()
+    assert h.gridadmm_config_preset(c, WORKLOAD["preset"].encode()) == 0
+    for k, v in (("max_outer", 1), ("max_inner", warmup + steps), ("workers", workers)):
+        assert h.gridadmm_config_set(c, k.encode(), float(v)) == 0, k
+    rep = ctypes.c_void_p()
     t0 = time.perf_counter()
-    series, info, _ = ref.solve(rho_pq=c["rho_pq"], rho_va=c["rho_va"], max_outer=1,
-                                max_inner=n, workers=workers)
+    st = h.gridadmm_solve(net, c, ctypes.byref(rep))
     wall = time.perf_counter() - t0
+    if st not in (0, 4):
+        raise RuntimeError(f"reference solve status {st}: {h.gridadmm_last_error().decode()}")
+    with tempfile.TemporaryDirectory() as td:
+        csv = os.path.join(td, "convergence.csv")
+        assert h.gridadmm_report_write_convergence(rep, os.fsencode(csv)) == 0
+        series = np.loadtxt(csv, delimiter=",", skiprows=1, ndmin=2)
+    h.gridadmm_report_free(rep)
+    h.gridadmm_config_free(c)
+    h.gridadmm_network_free(net)
     el = series[:, 5]
-    start = el[args.warmup - 1] if args.warmup > 0 else 0.0
-    dt = el[n - 1] - start
-    return iters_timed / dt, dt, wall, series
+    start = el[warmup - 1] if warmup > 0 else 0.0
+    dt = float(el[warmup + steps - 1] - start)
+    return steps / dt, dt, wall, series, dims
 
 
 def run_reference_arm(args, d: Dist):
     if d.rank != 0:
         return
-    path = case_file(args.shape, args.seed, d) if d.world == 1 else None
-    if path is None:
-        from paper_2110_06879_b200 import synth
-        path = synth.ensure_case(args.shape, "/tmp/gridadmm_cases", seed=args.seed)
+    from gridcases import synth
+    path = synth.ensure_case(WORKLOAD["shape"], "/tmp/gridadmm_cases", seed=WORKLOAD["seed"])
     workers = os.cpu_count() or 1
-    rate, dt, wall, _ = reference_rate(path, args, args.steps, workers)
+    rate, dt, wall, _, dims = reference_run(path, args.warmup, args.steps, workers)
+    sample = (f"inner iterations {args.warmup}..{args.warmup + args.steps - 1} of the cold "
+              f"start, reference C++ solver (oracle/_ref, unmodified sources) via its C ABI, "
+              f"workers={workers}; {dt:.1f} s of {wall:.1f} s wall")
     line = {
-        "metric": "ADMM iters/sec & time-to-converge (s) on ACTIVSg70k; warm-start track s/step",
-        "impl": "reference", "value": rate, "unit": "iters/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / rate,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded tiling of MATPOWER case30/case118 to ACTIVSg70k dims)",
-        "config": {"workload": f"{args.shape}-shaped cold start, inner iterations "
-                               f"{args.warmup}..{args.warmup + args.steps - 1}",
-                   "preset": args.preset, "seed": args.seed},
+        "metric": METRIC, "impl": "reference", "value": rate, "unit": "iters/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 / rate, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": DATA,
+        "config": workload_config(args, dims),
         "cpu_baseline": {"value": rate, "unit": "iters/s", "cores": workers, "kind": "reference",
-                         "sample": f"{args.steps} timed inner iterations after {args.warmup} "
-                                   f"warm-up, reference C++ solver, workers={workers}"},
+                         "sample": sample},
         "e2e": {"value": rate, "unit": "iters/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def run_b200_partitioned(args, d: Dist, ga, path, net):
-    """N > 1: one ACTIVSg70k-shaped grid split over N GPUs by the bus-graph
-    partition (strong scaling); every step is one ADMM iteration of the whole
-    grid, boundary rows and residual norms exchanged with NCCL inside the
-    library.  Device time per step from CUDA events on each rank's stream,
-    max over ranks."""
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+def run_b200_partitioned(args, d: Dist, ga, net):
+    """N > 1: one grid split over N GPUs by the bus-graph partition (strong
+    scaling); every step is one ADMM iteration of the whole grid, boundary
+    rows and residual norms exchanged with NCCL inside the library.  Device
+    time per step from CUDA events on each rank's stream, max over ranks."""
     dev = d.local
-    cfg = ga.Config(args.preset, device=dev)
+    cfg = ga.Config(WORKLOAD["preset"], device=dev)
     nccl_id = d.bcast(ga.nccl_unique_id() if d.rank == 0 else None)
     sess = ga.Session.distributed(net, cfg, d.rank, d.world, nccl_id)
     sess.timed_steps(args.warmup, 0)
@@ -256,122 +294,111 @@ def run_b200_partitioned(args, d: Dist, ga, path, net):
     d.barrier()
     max_ms = d.max(float(np.sum(step_ms)))
     value = args.steps / (max_ms * 1e-3)
-    # e2e: open a fresh partitioned session (network + cold-start state upload,
-    # NCCL communicator) and run W+K iterations, host wall clock, max over ranks
-    n_e2e = max(args.warmup + args.steps, 200)
+    # e2e: a fresh partitioned session (network + cold-start state upload,
+    # NCCL communicator) running W+K iterations, host wall clock, max over ranks
+    n_e2e = args.warmup + args.steps
     nccl_id2 = d.bcast(ga.nccl_unique_id() if d.rank == 0 else None)
     d.barrier()
     t0 = time.perf_counter()
     s2 = ga.Session.distributed(net, cfg, d.rank, d.world, nccl_id2)
     rec2, _ = s2.iterate(n_e2e)
     t_e2e = d.max(time.perf_counter() - t0)
-    nb, ng, nl, m = net.num_buses, net.num_generators, net.num_branches, net.num_rows
-    conv = None
-    if d.rank == 0 and d.world == 1 and not args.no_converge:
-        try:
-            conv = run_converge(args, ga, net, path, dev)
-        except Exception as e:  # noqa: BLE001
-            conv = {"failed": str(e)}
-
+    dims = (net.num_buses, net.num_generators, net.num_branches)
     if d.rank == 0:
         line = {
-            "metric": "ADMM iters/sec & time-to-converge (s) on ACTIVSg70k; warm-start track s/step",
-            "value": value, "unit": "iters/s", "n_gpus": d.world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded tiling of MATPOWER case30/case118 to ACTIVSg70k dims)",
-            "config": {"workload": f"{args.shape}-shaped ({nb} buses, {ng} gens, {nl} branches, "
-                                   f"m={m}) cold start, inner iterations "
-                                   f"{args.warmup}..{args.warmup + args.steps - 1}",
-                       "preset": args.preset, "seed": args.seed,
-                       "l2": "flushed between steps (256 MiB write outside the timed events)",
-                       "parallelism": f"bus-graph partition over {d.world} GPUs, NCCL boundary "
-                                      f"exchange"},
-            "roofline": {"bound": "fp64", "kernel": "branch NLP kernels", "achieved": None,
-                         "peak": None, "unit": "TFLOP/s", "frac": None, "traffic": None,
+            "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": d.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": DATA,
+            "config": dict(workload_config(args, dims),
+                           parallelism=f"bus-graph partition over {d.world} GPUs, NCCL boundary "
+                                       f"exchange"),
+            "roofline": {"bound": "fp64", "achieved": None, "peak": None, "unit": "TFLOP/s",
+                         "frac": None, "traffic": None,
                          "note": "per-kernel roofline is measured in the N=1 run"},
             "e2e": {"value": len(rec2) / t_e2e, "unit": "iters/s", "wall_s": t_e2e,
                     "iterations": int(len(rec2)), "h2d_bytes_per_step": None,
                     "d2h_bytes_per_step": 56,
                     "note": "gridadmm_session_new_dist (upload, NCCL init) + iterate, max over ranks"},
             "cpu_baseline": None,
-            "gpu_launches": 10 * args.steps,
+            "gpu_launches": 6 * args.steps,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
 
 
-def run_converge(args, ga, net, path, dev):
-    """Time-to-converge of a cold start (eps 1e-4, 20 x 1000 iterations) on
-    the device, driven exactly like driver.cpp:152-239 (inner loops with the
-    reference's stop tests inside gridadmm_session_iterate, outer updates
-    with the beta schedule), wall clock from session creation.  At the start
-    of outer iteration LATE_OUTER the full state is snapshotted (excluded
-    from the wall time); from it the reference C++ solver (all host cores)
-    and a fresh device session each run LATE_STEPS iterations: the late-solve
-    rate of both, with bit-identical residual series."""
-    import oracle
-    eps, max_inner, max_outer = 1e-4, 1000, 20
-    cfg = ga.Config(rho_pq=CONVERGE_RHO[0], rho_va=CONVERGE_RHO[1], eps=eps, device=dev,
-                    max_inner=max_inner, max_outer=max_outer)
+def run_converge(ga, net, dev):
+    """Full cold start through gridadmm_solve (driver.cpp:140-246 stop rules),
+    preset penalties, default eps 1e-4 / 20 x 1000 iterations; wall clock of
+    the call; the reference's quality metrics of the returned solution."""
+    cfg = ga.Config(WORKLOAD["preset"], device=dev)
     t0 = time.perf_counter()
-    paused = 0.0
-    s = ga.Session(net, cfg)
-    prev, status, iters, snap, outer = -1.0, "ERR_ITERATION_LIMIT", 0, None, 0
-    for outer in range(1, max_outer + 1):
-        if outer == LATE_OUTER:
-            tp = time.perf_counter()
-            snap = (s.get_state(), iters)
-            paused += time.perf_counter() - tp
-        rec, why = s.iterate(max_inner)
-        iters += len(rec)
-        if why == 2:
-            status = "ERR_DIVERGED"
-            break
-        z = float(rec[-1, 2])
-        if z <= eps:
-            status = "OK"
-            break
-        s.phase("outer", z, prev)
-        prev = z
-    wall = time.perf_counter() - t0 - paused
-    s.close()
-    out = {"time_to_converge_s": wall, "status": status, "inner_iterations": iters,
-           "outer_iterations": outer, "iters_per_s": iters / wall,
-           "rho": list(CONVERGE_RHO), "eps": eps,
-           "note": "device session driven with driver.cpp's loop control; wall clock incl. setup"}
-    if snap is not None and oracle.have_ref():
-        st, at = snap
-        s2 = ga.Session(net, cfg)
-        s2.set_state(st)
-        ms, rec = s2.timed_steps(LATE_STEPS, L2_FLUSH_BYTES)
-        s2.close()
-        workers = os.cpu_count() or 1
-        ref = oracle.RefNet(path)
-        series, _, _ = ref.solve(init=st, rho_pq=CONVERGE_RHO[0], rho_va=CONVERGE_RHO[1], eps=eps,
-                                 max_outer=1, max_inner=LATE_STEPS, workers=workers)
-        el = series[:, 5]
-        gpu_rate = LATE_STEPS / (float(np.sum(ms)) * 1e-3)
-        cpu_rate = LATE_STEPS / float(el[-1]) if el[-1] > 0 else None
-        out["late_window"] = {
-            "start_iteration": at, "beta": float(st["beta"][0]), "steps": LATE_STEPS,
-            "gpu_iters_per_s": gpu_rate, "cpu_iters_per_s": cpu_rate, "cpu_cores": workers,
-            "gpu_over_cpu": gpu_rate / cpu_rate if cpu_rate else None,
-            "residuals_bit_identical": bool(np.array_equal(
-                series[:LATE_STEPS, 2:5].view(np.uint64), rec[:LATE_STEPS, 0:3].view(np.uint64)))}
+    st, rep = ga.solve(net, cfg)
+    wall = time.perf_counter() - t0
+    m = rep.metrics()
+    rep.close()
+    out = {"time_to_converge_s": wall, "status": ga.STATUS[st],
+           "inner_iterations": int(m["inner_iterations"]),
+           "outer_iterations": int(m["outer_iterations"]),
+           "iters_per_s": m["inner_iterations"] / wall, "c_inf": m["c_inf"],
+           "balance_inf": m["balance_inf"], "limit_violation": m["limit_violation"],
+           "bound_violation": m["bound_violation"], "objective": m["objective"],
+           "eps": cfg["eps"], "rho": [cfg["rho_pq"], cfg["rho_va"]],
+           "note": "gridadmm_solve on a loaded network, wall clock incl. device setup"}
+    ref = _load_json(CPU_FULL_SOLVE_FILE)
+    if ref:
+        out["cpu_full_solve_s"] = ref.get("cpu_time_s")
+        out["cpu_full_solve_cores"] = ref.get("cpu_cores")
+        out["cpu_full_solve_iterations"] = ref.get("cpu_inner")
+        out["cpu_full_solve_source"] = os.path.relpath(CPU_FULL_SOLVE_FILE, REPO)
+        out["cpu_objective_bit_identical"] = (
+            ref.get("cpu_objective_hex") == float(m["objective"]).hex())
+        if ref.get("cpu_time_s"):
+            out["speedup_vs_cpu_full_solve"] = ref["cpu_time_s"] / wall
+    return out
+
+
+def run_track(ga, dev):
+    """Warm-start tracking, BASELINE configs[4]: ACTIVSg25k-shaped grid,
+    30 snapshots (gridcases.synth.ensure_profile), ramp_frac 0.02, preset
+    case_ACTIVSg25k; seconds per warm snapshot through gridadmm_track_run."""
+    from gridcases import synth
+    path = synth.ensure_case("case_ACTIVSg25k", "/tmp/gridadmm_cases")
+    net = ga.Network(path)
+    prof = synth.ensure_profile(path, periods=30)
+    cfg = ga.Config("case_ACTIVSg25k", device=dev, ramp_frac=0.02)
+    t0 = time.perf_counter()
+    st, trk = ga.track(net, cfg, prof)
+    wall = time.perf_counter() - t0
+    per = trk.period_table()
+    trk.close()
+    warm = [p["time_s"] for p in per[1:]]
+    out = {"workload": "case_ACTIVSg25k-shaped, 30 snapshots: per-bus multipliers "
+                       "P(t)(1+eps), P(t) 1-minute interpolation of an hourly series "
+                       "(<=5% swing), eps~N(0,0.005^2); ramp_frac 0.02; gridadmm_track_run",
+           "status": ga.STATUS[st], "periods": len(per), "wall_s": wall,
+           "cold_s": per[0]["time_s"] if per else None,
+           "warm_s_per_step_mean": float(np.mean(warm)) if warm else None,
+           "warm_s_per_step_max": float(np.max(warm)) if warm else None,
+           "warm_inner_mean": float(np.mean([p["inner"] for p in per[1:]])) if warm else None,
+           "c_inf_max": float(max(p["c_inf"] for p in per)) if per else None}
+    ref = _load_json(TRACK_CPU_FILE)
+    if ref:
+        out["cpu_warm_s_per_step_mean"] = ref.get("cpu_warm_s_per_step_mean")
+        out["cpu_cores"] = ref.get("cpu_cores")
+        out["cpu_source"] = os.path.relpath(TRACK_CPU_FILE, REPO)
     return out
 
 
 def run_b200(args, d: Dist):
     import paper_2110_06879_b200 as ga
-    path = case_file(args.shape, args.seed, d)
+    path = case_file(d)
     dev = d.local
     net = ga.Network(path)
-    cfg = ga.Config(args.preset, device=dev)
-    nb, ng, nl, m = net.num_buses, net.num_generators, net.num_branches, net.num_rows
-
     if d.world > 1 or os.environ.get("GRIDADMM_BENCH_DIST") == "1":
-        return run_b200_partitioned(args, d, ga, path, net)
+        return run_b200_partitioned(args, d, ga, net)
+    cfg = ga.Config(WORKLOAD["preset"], device=dev)
+    nb, ng, nl, m = net.num_buses, net.num_generators, net.num_branches, net.num_rows
 
     # --- device-resident timed region -----------------------------------
     sess = ga.Session(net, cfg)
@@ -384,10 +411,9 @@ def run_b200(args, d: Dist):
     d.barrier()
     k1 = [sess.kernel_time(c) for c in range(6)]
     it1 = sess.step_counters()
-    my_ms = float(np.sum(step_ms))
-    max_ms = d.max(my_ms)
-    total_iters = d.sum(float(args.steps))
-    value = total_iters / (max_ms * 1e-3)
+    sess.close()
+    max_ms = d.max(float(np.sum(step_ms)))
+    value = args.steps / (max_ms * 1e-3)
 
     kern = {name: {"ms_total": k1[c][0] - k0[c][0], "launches": k1[c][1] - k0[c][1]}
             for c, name in enumerate(["generators", "branches", "buses", "zy", "branch_lane_phase",
@@ -399,124 +425,127 @@ def run_b200(args, d: Dist):
     tron4, tron6 = it1[0] - it0[0], it1[1] - it0[1]
     exec4, exec6 = it1[2] - it0[2], it1[3] - it0[3]
     branch_ms = kern["branches"]["ms_total"]
-    flops = exec4 * CENSUS_FLOPS[4] + exec6 * CENSUS_FLOPS[6]
-    ref_flops = tron4 * CENSUS_FLOPS[4] + tron6 * CENSUS_FLOPS[6]
+    census = _load_json(CENSUS_FILE) or {}
+    per4 = census.get("per_iter4", CENSUS_FLOPS[4])
+    per6 = census.get("per_iter6", CENSUS_FLOPS[6])
+    flops = exec4 * per4 + exec6 * per6
+    ref_flops = tron4 * per4 + tron6 * per6
     fp64_mul_add, fp64_fma = ga.fp64_peak(dev)
     achieved = flops / (branch_ms * 1e-3) / 1e12 if branch_ms > 0 else 0.0
-    # HBM-bound phases: algorithmic bytes per iteration
-    # generators: 4 row arrays x 2 rows + 6 params read, 2 rows written;
-    # buses (fused with z / y / norms): per row the CSR index + rho, x, z, y,
-    # xbar, lambda read and xbar, z, y written (76 B), per bus 7 CSR offsets
-    # + gs, bs, pd, qd read and w, theta written (76 B)
+    # HBM-bound kernels: algorithmic bytes per iteration
     hbm_bytes = {"generators": 128 * ng, "buses": 76 * m + 76 * nb}
+    peaks = _load_json(os.path.join(REPO, "MEASURED_PEAKS.json")) or {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
     hbm = {}
     for name, b in hbm_bytes.items():
         t = kern[name]["ms_total"] / max(1, kern[name]["launches"])
-        hbm[name] = {"gbs": b / (t * 1e-3) / 1e9 if t > 0 else None, "bytes": b, "ms": t}
-    peaks = {}
+        gbs = b / (t * 1e-3) / 1e9 if t > 0 else None
+        hbm[name] = {"achieved_gbs": gbs, "bytes": b, "ms": t, "peak_gbs": hbm_peak,
+                     "frac": gbs / hbm_peak if gbs else None}
+    # DRAM traffic per launch of the dominant kernel and the executed FP64
+    # instruction counts, from the committed ncu capture of this workload
+    traffic, traffic_note, ncu_fp64 = None, None, None
     try:
-        peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    # DRAM traffic per launch of the dominant kernel from the committed ncu
-    # --set full capture (profiles/r01_ncu_traffic.jsonl, inner iteration 10)
-    traffic, traffic_note = None, None
-    try:
-        unit = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-        for ln in open(os.path.join(REPO, "profiles", "r01_ncu_traffic.jsonl")):
+        for ln in open(NCU_TRAFFIC_FILE):
             t = json.loads(ln)
-            if t["kernel"] == "lane_kernel":
-                traffic = t["dram_read"][0] * unit[t["dram_read"][1]] + \
-                    t["dram_write"][0] * unit[t["dram_write"][1]]
+            if t.get("kernel") == "lane_kernel" and "dram_bytes" in t:
+                traffic = t["dram_bytes"]
                 traffic_note = ("lane_kernel dram__bytes_read+write per launch, ncu --set full, "
-                                "profiles/r01_ncu_traffic.jsonl; the phase is FP64-latency bound")
+                                + os.path.relpath(NCU_TRAFFIC_FILE, REPO))
+            if t.get("kernel") == "branch_phase_fp64":
+                ncu_fp64 = t
     except Exception:  # noqa: BLE001
         pass
 
     # --- e2e through the C ABI (host buffers) -----------------------------
     e2e = None
     if not args.no_e2e:
-        n_e2e = max(args.warmup + args.steps, 200)
-        cfg2 = ga.Config(args.preset, device=dev, max_outer=1, max_inner=n_e2e)
+        n_e2e = max(args.warmup + args.steps, 200)  # amortizes device setup like a real solve
+        cfg2 = ga.Config(WORKLOAD["preset"], device=dev, max_outer=1, max_inner=n_e2e)
         net2 = ga.Network(path)  # host parse (file I/O) outside, like the reference's elapsed_s
         d.barrier()
         t0 = time.perf_counter()
-        st, rep = ga.solve(net2, cfg2)  # network + state H2D, iterations, solution D2H
+        st, rep = ga.solve(net2, cfg2)  # network H2D, cold start, iterations, solution D2H
         pg, qg = rep.dispatch()
         vm, va = rep.voltages()
         t_e2e = time.perf_counter() - t0
         n_it = rep.metric("inner_iterations")
+        rep.close()
+        net2.close()
         t_max = d.max(t_e2e)
-        h2d = (8 * (6 * ng + 10 * nl + 6 * nb) + 4 * (3 * nl + 7 * nb + m)  # network
-               + 8 * (6 * m + 2 * nb + 9 * nl))  # cold-start state
+        h2d = (8 * (6 * ng + 10 * nl + 6 * nb) + 4 * (3 * nl + 7 * nb + m))  # network SoA
         d2h = 56 * n_it + 8 * (2 * ng + 2 * nb)
-        e2e = {"value": d.sum(n_it) / t_max, "unit": "iters/s",
+        e2e = {"value": n_it / t_max, "unit": "iters/s",
                "h2d_bytes_per_step": h2d / n_it, "d2h_bytes_per_step": d2h / n_it,
                "wall_s": t_max, "iterations": int(n_it),
-               "note": "gridadmm_solve(max_outer=1) on a loaded network + dispatch/voltages: "
-                       "device alloc, network+state upload, cold start, every iteration's "
-                       "norm readback, solution download (file parse excluded)"}
+               "note": "gridadmm_solve(max_outer=1, max_inner=max(W+K, 200)) on a loaded network + "
+                       "dispatch/voltages: device alloc, network upload, device cold start, "
+                       "every iteration's norm readback, solution download (file parse excluded)"}
 
     # --- CPU baseline (reference on host cores), rank 0 only ---------------
     cpu = None
-    if d.rank == 0 and d.world == 1 and not args.no_cpu_baseline:
+    if d.rank == 0 and not args.no_cpu_baseline:
         workers = os.cpu_count() or 1
         ksteps = min(args.cpu_steps, args.steps)
         try:
-            rate, dt, wall, series = reference_rate(path, args, ksteps, workers)
-            # same trajectory: the reference's residuals must equal ours bit-for-bit
-            same = bool(np.array_equal(series[args.warmup:args.warmup + ksteps, 2:5].view(np.uint64),
-                                       rec[:ksteps, 0:3].view(np.uint64)))
+            rate, dt, wall, series, _ = reference_run(path, args.warmup, ksteps, workers)
+            same = bool(np.array_equal(
+                series[args.warmup:args.warmup + ksteps, 2:5].view(np.uint64),
+                rec[:ksteps, 0:3].view(np.uint64)))
             cpu = {"value": rate, "unit": "iters/s", "cores": workers, "kind": "reference",
                    "sample": f"inner iterations {args.warmup}..{args.warmup + ksteps - 1} of the "
                              f"same cold start ({dt:.1f} s of {wall:.1f} s wall), reference C++ "
-                             f"solver from oracle/_ref, workers={workers}",
+                             f"solver (oracle/_ref) via its C ABI, workers={workers}",
                    "residuals_bit_identical_to_gpu": same}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "iters/s", "cores": workers, "kind": "reference",
                    "sample": f"failed: {e}"}
 
     conv = None
-    if d.rank == 0 and d.world == 1 and not args.no_converge:
+    if d.rank == 0 and not args.no_converge:
         try:
-            conv = run_converge(args, ga, net, path, dev)
+            conv = run_converge(ga, net, dev)
         except Exception as e:  # noqa: BLE001
             conv = {"failed": str(e)}
+    track = None
+    if d.rank == 0 and not args.no_track:
+        try:
+            track = run_track(ga, dev)
+        except Exception as e:  # noqa: BLE001
+            track = {"failed": str(e)}
 
     if d.rank == 0:
         line = {
-            "metric": "ADMM iters/sec & time-to-converge (s) on ACTIVSg70k; warm-start track s/step",
-            "value": value, "unit": "iters/s", "n_gpus": d.world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded tiling of MATPOWER case30/case118 to ACTIVSg70k dims)",
-            "config": {"workload": f"{args.shape}-shaped ({nb} buses, {ng} gens, {nl} branches, "
-                                   f"m={m}) cold start, inner iterations "
-                                   f"{args.warmup}..{args.warmup + args.steps - 1}",
-                       "preset": args.preset, "seed": args.seed,
-                       "l2": "flushed between steps (256 MiB write outside the timed events)",
-                       "parallelism": "replicas" if d.world > 1 else "single GPU"},
+            "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": d.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": DATA,
+            "config": workload_config(args, (nb, ng, nl)),
             "roofline": {"bound": "fp64",
                          "kernel": "branch phase: lane_kernel + tile_kernel + solo_kernel (TRON NLPs)",
                          "achieved": achieved, "peak": fp64_mul_add, "unit": "TFLOP/s",
                          "frac": achieved / fp64_mul_add if fp64_mul_add else None,
                          "traffic": traffic, "traffic_note": traffic_note,
-                         "peak_note": "measured DMUL+DADD issue rate (kernel built -fmad=false); "
+                         "peak_note": "measured DMUL+DADD issue rate on this GPU "
+                                      "(gridadmm_probe_fp64_peak; kernels built -fmad=false); "
                                       f"DFMA peak {fp64_fma:.1f} TFLOP/s",
                          "flops_per_launch": flops / max(1, kern["branches"]["launches"]),
+                         "census_flops_per_tron_iteration": {"n4": per4, "n6": per6,
+                                                             "source": census.get("source")},
                          "tron_iterations_reference": [tron4, tron6],
                          "tron_steps_executed": [exec4, exec6],
+                         "ncu_executed_fp64": ncu_fp64,
                          "reference_equivalent_tflops": (ref_flops / (branch_ms * 1e-3) / 1e12
                                                          if branch_ms > 0 else None)},
-            "roofline_hbm": {k: dict(v, peak_gbs=hbm_peak,
-                                     frac=(v["gbs"] / hbm_peak if v["gbs"] else None))
-                             for k, v in hbm.items()},
+            "roofline_hbm": hbm,
             "kernels": kern,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "converge": conv,
+            "track": track,
             "gpu_launches": 6 * args.steps,
+            "gpu_launches_note": "per step: reset_scalars, gen_kernel, lane_kernel, tile_kernel, "
+                                 "solo_kernel, bus_block_kernel (the L2-flush memset excluded)",
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

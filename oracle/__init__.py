@@ -188,23 +188,79 @@ class RefNet:
         return series[: 6 * k].reshape(-1, 6), info, fin
 
 
+# The reference's C ABI (proj/include/gridadmm/gridadmm.h:33-101), typed here
+# so the oracle never imports the product package.
+_S, _I = ctypes.c_char_p, ctypes.c_int
+REF_SYMBOLS = {
+    "gridadmm_last_error": (_S, []),
+    "gridadmm_network_load": (_I, [_S, ctypes.POINTER(_P)]),
+    "gridadmm_network_free": (None, [_P]),
+    "gridadmm_network_num_buses": (_I, [_P]),
+    "gridadmm_network_num_generators": (_I, [_P]),
+    "gridadmm_network_num_branches": (_I, [_P]),
+    "gridadmm_config_new": (_P, []),
+    "gridadmm_config_free": (None, [_P]),
+    "gridadmm_config_set": (_I, [_P, _S, _D]),
+    "gridadmm_config_get": (_I, [_P, _S, _DP]),
+    "gridadmm_config_preset": (_I, [_P, _S]),
+    "gridadmm_solve": (_I, [_P, _P, ctypes.POINTER(_P)]),
+    "gridadmm_report_free": (None, [_P]),
+    "gridadmm_report_metric": (_I, [_P, _S, _DP]),
+    "gridadmm_report_dispatch": (_I, [_P, _DP, _DP]),
+    "gridadmm_report_voltages": (_I, [_P, _DP, _DP]),
+    "gridadmm_report_write_solution": (_I, [_P, _S, _D]),
+    "gridadmm_report_write_convergence": (_I, [_P, _S]),
+    "gridadmm_track_run": (_I, [_P, _P, _S, ctypes.POINTER(_P)]),
+    "gridadmm_track_free": (None, [_P]),
+    "gridadmm_track_num_periods": (_I, [_P]),
+    "gridadmm_track_period_report": (_I, [_P, _I, ctypes.POINTER(_P)]),
+    "gridadmm_track_write_periods": (_I, [_P, _S, _DP, _I]),
+}
+METRIC_KEYS = ("objective", "balance_inf", "limit_violation", "bound_violation", "c_inf",
+               "outer_iterations", "inner_iterations", "branch_solve_failures")
+
+
 def ref_capi():
     """The reference's own C ABI (the 23 gridadmm_* symbols of
-    proj/include/gridadmm/gridadmm.h) from _ref/libgridadmm_ref.so, typed like
-    the product binding so reports can be compared call for call."""
-    import paper_2110_06879_b200 as ga
+    proj/include/gridadmm/gridadmm.h) from _ref/libgridadmm_ref.so."""
     h = RefLib.get()
-    for name, (res, args) in ga.SYMBOLS.items():
+    for name, (res, args) in REF_SYMBOLS.items():
         fn = getattr(h, name)
         fn.restype = res
         fn.argtypes = args
     return h
 
 
+def ref_metrics(h, rep) -> Dict[str, float]:
+    out = {}
+    for key in METRIC_KEYS:
+        v = ctypes.c_double()
+        h.gridadmm_report_metric(rep, key.encode(), ctypes.byref(v))
+        out[key] = v.value
+    return out
+
+
+def ref_preset(name: str):
+    """(rho_pq, rho_va) of a named preset, from the reference's own table
+    (capi.cpp:25-39) through gridadmm_config_preset."""
+    h = ref_capi()
+    c = h.gridadmm_config_new()
+    try:
+        if h.gridadmm_config_preset(c, name.encode()) != 0:
+            raise KeyError(name)
+        out = []
+        for key in ("rho_pq", "rho_va"):
+            v = ctypes.c_double()
+            h.gridadmm_config_get(c, key.encode(), ctypes.byref(v))
+            out.append(v.value)
+        return tuple(out)
+    finally:
+        h.gridadmm_config_free(c)
+
+
 def ref_track(case_path: str, profile_csv: str, preset: str, **cfg):
     """gridadmm_track_run through the reference's C ABI; returns a list of
     per-period metric dicts and the status."""
-    import paper_2110_06879_b200 as ga
     h = ref_capi()
     net = ctypes.c_void_p()
     assert h.gridadmm_network_load(os.fsencode(case_path), ctypes.byref(net)) == 0
@@ -215,14 +271,20 @@ def ref_track(case_path: str, profile_csv: str, preset: str, **cfg):
     trk = ctypes.c_void_p()
     st = h.gridadmm_track_run(net, c, os.fsencode(profile_csv), ctypes.byref(trk))
     out = []
+    if not trk.value:
+        h.gridadmm_config_free(c)
+        h.gridadmm_network_free(net)
+        return st, out
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        csv = os.path.join(td, "periods.csv")
+        assert h.gridadmm_track_write_periods(trk, os.fsencode(csv), None, 0) == 0
+        times = np.genfromtxt(csv, delimiter=",", names=True, ndmin=1)["time_s"]
     for p in range(1, h.gridadmm_track_num_periods(trk) + 1):
         rep = ctypes.c_void_p()
         assert h.gridadmm_track_period_report(trk, p, ctypes.byref(rep)) == 0
-        m = {}
-        for key in ga.METRIC_KEYS:
-            v = ctypes.c_double()
-            h.gridadmm_report_metric(rep, key.encode(), ctypes.byref(v))
-            m[key] = v.value
+        m = ref_metrics(h, rep)
+        m["time_s"] = float(times[p - 1])
         out.append(m)
         h.gridadmm_report_free(rep)
     h.gridadmm_track_free(trk)

@@ -319,6 +319,17 @@ class Tracking:
         _check(lib().gridadmm_track_write_periods(self._h, os.fsencode(path),
                                                   _dp(arr) if arr.size else None, int(arr.size)))
 
+    def period_table(self):
+        """Per-period rows of periods.csv (outputs.cpp:122-135): period,
+        inner iterations, solve seconds, c_inf."""
+        import tempfile
+        with tempfile.TemporaryDirectory() as td:
+            path = os.path.join(td, "periods.csv")
+            self.write_periods(path)
+            rows = np.genfromtxt(path, delimiter=",", names=True, ndmin=1)
+        return [{"period": int(r["period"]), "inner": int(r["inner_iters"]),
+                 "time_s": float(r["time_s"]), "c_inf": float(r["viol_inf"])} for r in rows]
+
     def close(self):
         if getattr(self, "_h", None):
             lib().gridadmm_track_free(self._h)

@@ -8,7 +8,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import oracle  # noqa: E402
 import paper_2110_06879_b200 as ga  # noqa: E402
-from paper_2110_06879_b200 import synth  # noqa: E402
+from gridcases import synth  # noqa: E402
 
 shape = sys.argv[1] if len(sys.argv) > 1 else "case_ACTIVSg70k"
 preset = sys.argv[2] if len(sys.argv) > 2 else "case_ACTIVSg70k"

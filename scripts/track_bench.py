@@ -12,7 +12,7 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import paper_2110_06879_b200 as ga  # noqa: E402
-from paper_2110_06879_b200 import synth  # noqa: E402
+from gridcases import synth  # noqa: E402
 
 
 def write_profile(net, periods, path, seed=25, swing=0.05, noise=0.005):

@@ -199,7 +199,7 @@ def test_series_parity_synthetic_scale(gridadmm, oracle_mod, shape, lane_budget)
     branch phases, both tile widths side by side in one tile kernel, the
     block-staged bus kernel with multi-block staging) vs the reference, for
     two device runs with different lane budgets."""
-    from paper_2110_06879_b200 import synth
+    from gridcases import synth
     import os
     iters = 30
     path = synth.ensure_case(shape, "/tmp/gridadmm_cases")

@@ -119,7 +119,7 @@ def test_layout_matches_reference(gridadmm, oracle_mod, name):
 
 
 def test_synthetic_case_shapes_and_determinism(gridadmm, tmp_path, oracle_mod):
-    from paper_2110_06879_b200 import synth
+    from gridcases import synth
     p1 = synth.write_case("case2868rte", str(tmp_path / "a.m"), seed=5)
     p2 = synth.write_case("case2868rte", str(tmp_path / "b.m"), seed=5)
     assert open(p1).read() == open(p2).read()

@@ -124,7 +124,7 @@ def test_partitioned_full_solve_case9(gridadmm):
 
 @pytest.mark.gpu
 def test_partitioned_synthetic_grid(gridadmm):
-    from paper_2110_06879_b200 import synth
+    from gridcases import synth
     path = synth.ensure_case("case2868rte", "/tmp/gridadmm_cases")
     net = gridadmm.Network(path)
     s1 = gridadmm.Session(net, gridadmm.Config("case_ACTIVSg70k"))

@@ -120,9 +120,13 @@ enum AlAction : int { kAlContinue = 0, kAlDone = 1, kAlFailed = 2 };
 
 // A TRON solve ended with `status`: AL bookkeeping of kernels.cpp:246-271.
 // Either restarts TRON for the next AL round (kAlContinue) or ends the branch.
+// `share` is the mask of the lanes that share `slot` (a tile) or 0 when the
+// slot is the lane's own: every sharer reads the multipliers before any of
+// them writes, so no lane can see an already-updated value.
 template <int N, int S, class BP>
 __device__ __forceinline__ int al_after_solve(int status, Slot<S> slot, const BP& p,
-                                              TronState<N>& ts, int& al_it, double& prev_res) {
+                                              TronState<N>& ts, int& al_it, double& prev_res,
+                                              unsigned share) {
     for (;;) {
         if (status == kTronNumericalError) return kAlFailed;
         if constexpr (N == 4) {
@@ -135,11 +139,15 @@ __device__ __forceinline__ int al_after_solve(int status, Slot<S> slot, const BP
             const double res = smax(fabs(rij), fabs(rji));
             if (res <= kAlTol) return kAlDone;
             const double rho_t = slot(F_RHOT);
-            const double lij = sclamp(slot(F_LTIJ) + rho_t * rij, -kLtBound, kLtBound);
-            const double lji = sclamp(slot(F_LTJI) + rho_t * rji, -kLtBound, kLtBound);
+            const double lt_ij = slot(F_LTIJ);
+            const double lt_ji = slot(F_LTJI);
+            if (share) __syncwarp(share);
+            const double lij = sclamp(lt_ij + rho_t * rij, -kLtBound, kLtBound);
+            const double lji = sclamp(lt_ji + rho_t * rji, -kLtBound, kLtBound);
             slot.set(F_LTIJ, lij);
             slot.set(F_LTJI, lji);
             if (res > kAlShrink * prev_res) slot.set(F_RHOT, smin(10.0 * rho_t, kRhoTildeMax));
+            if (share) __syncwarp(share);
             prev_res = res;
             if (++al_it >= kMaxAl) return kAlDone;
             if (tron_begin<N>(p, ts)) return kAlContinue;
@@ -200,11 +208,7 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
     const int lane = threadIdx.x & 31;
     unsigned my_exec = 0;  // trust-region steps executed by this lane
     const Slot<kLaneBlock> slot{smem + threadIdx.x};
-#ifndef GA_LANE_HESS_SMEM
-#define GA_LANE_HESS_SMEM 0
-#endif
-    // GA_LANE_HESS_SMEM: Hessian in the slot (HessSmem); measured neutral at 70k
-    BranchProb<N, kLaneBlock, GA_LANE_HESS_SMEM != 0> p{slot};
+    BranchProb<N, kLaneBlock> p{slot};
     const TronParams tp = tron_params(cfg);
     const double kInf = __longlong_as_double(0x7ff0000000000000LL);
 
@@ -244,7 +248,7 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
                     prev_res = kInf;
                     if (!tron_begin<N>(p, ts)) {
                         const int act = al_after_solve<N>(kTronNumericalError, slot, p, ts, al_it,
-                                                          prev_res);
+                                                          prev_res, 0u);
                         end_branch(act);
                     }
                 } else {
@@ -270,7 +274,7 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
             if (r != kStepContinue) {
                 const int status = solve_status<N, kLaneBlock, SerialSearch>(r, iter_before, p, ts,
                                                                             tp, iters);
-                const int act = al_after_solve<N>(status, slot, p, ts, al_it, prev_res);
+                const int act = al_after_solve<N>(status, slot, p, ts, al_it, prev_res, 0u);
 #if defined(GA_TRON_STATS) || defined(GA_BRANCH_STEPS)
                 if (act != kAlContinue) st.br_cost[b] = steps + 1;
 #endif
@@ -343,9 +347,6 @@ __global__ void __launch_bounds__(kLaneBlock, GA_LANE_MINB) lane_kernel(DevNet n
 }
 
 // ---- phase B: tiles of kTile lanes per overflow branch ---------------------
-#ifndef GA_GH_CACHE
-#define GA_GH_CACHE 0  // tile / solo: reuse gradient + Hessian after rejected steps (measured slower)
-#endif
 // Budget > 0: a branch still running after `budget` steps here is saved and
 // pushed to the solo queue (solo / solo_count), resumed by the solo phase.
 template <int N, int T>
@@ -365,7 +366,7 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
     // warps of one block may run different T (tail mode is decided per
     // queue), and must not share a slot.
     const Slot<S> slot{smem + (threadIdx.x / T) * (T / kTile)};
-    BranchProb<N, S, false, GA_GH_CACHE != 0> p{slot};
+    BranchProb<N, S> p{slot};
     const TronParams tp = tron_params(cfg);
     const int count = *ovf_count;
     unsigned long long my_iters = 0;
@@ -383,7 +384,6 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
         ts.f = st.mig_f[b];
         ts.delta = st.mig_delta[b];
         ts.iter = st.mig_iter[b];
-        ts.ghc = false;  // the cache slot may hold another branch's values
         int al_it = st.mig_al[b];
         double prev_res = st.mig_prev_res[b];
         int iters = st.mig_cost[b];
@@ -421,7 +421,7 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
             ++branch_exec;
             if (r == kStepContinue) continue;
             const int status = solve_status<N, S, TileSearch<T>>(r, iter_before, p, ts, tp, iters);
-            act = al_after_solve<N>(status, slot, p, ts, al_it, prev_res);
+            act = al_after_solve<N>(status, slot, p, ts, al_it, prev_res, mask);
         }
         __syncwarp(mask);
         if (handed_off) continue;
@@ -442,7 +442,7 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
 
 __global__ void __launch_bounds__(kTileBlock, GA_TILE_MINB) tile_kernel(DevNet net, DevState st, BranchCfg cfg,
                                                           Work w, DevScalars* sc) {
-    __shared__ double smem[(GA_GH_CACHE ? kFieldsCache : kFields) * (kTileBlock / kTile)];
+    __shared__ double smem[kFields * (kTileBlock / kTile)];
     unsigned long long it6 = 0, it4 = 0;
     int fails = 0;
     // Tail mode: when a queue holds no more branches than half the grid's
@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(kTileBlock, GA_TILE_MINB) tile_kernel(DevNet n
 // diverging in the warp) in a block of its own.
 __global__ void __launch_bounds__(kSoloBlock) solo_kernel(DevNet net, DevState st, BranchCfg cfg,
                                                           Work w, DevScalars* sc) {
-    __shared__ double smem[(GA_GH_CACHE ? kFieldsCache : kFields) * (kTileBlock / kTile)];
+    __shared__ double smem[kFields * (kTileBlock / kTile)];
     unsigned long long it6 = 0, it4 = 0;
     int fails = 0;
     tile_phase<6, 32>(net, st, cfg, w.solo6, &w.ctr[6], &w.ctr[8], smem, &it6, &fails, &sc->exec6, 0,
@@ -510,14 +510,7 @@ __global__ void __launch_bounds__(kSoloBlock) solo_kernel(DevNet net, DevState s
 // Dense box QP for the TRON-core parity test (proj/tests/acceptance.cpp:458-520).
 template <int N>
 struct QpProb {
-    static constexpr bool kGhCache = false;
-    GA_FN double cache_g(int) const { return 0.0; }
-    GA_FN double cache_h(int) const { return 0.0; }
-    GA_FN void cache_put_g(int, double) const {}
-    GA_FN void cache_put_h(int, double) const {}
     const double *H, *G, *L, *U;
-    template <int NN>
-    GA_FN HessRegs<NN> hess_store() const { return HessRegs<NN>{}; }
     GA_FN double lo(int i) const { return L[i]; }
     GA_FN double hi(int i) const { return U[i]; }
     GA_FN double value(const double* x) const {
@@ -687,7 +680,7 @@ void launch_branches(const DevNet& n, const DevState& s, const BranchCfg& cfg, D
     const Work w = work_of(n, s);
     cudaMemsetAsync(w.ctr, 0, kCounters * sizeof(int), st);
     const size_t lane_smem =
-        static_cast<size_t>(GA_LANE_HESS_SMEM ? kFieldsHess : kFields) * kLaneBlock * sizeof(double);
+        static_cast<size_t>(kFields) * kLaneBlock * sizeof(double);
     // persistent grid sizes (thread-safe one-time init; the pool's GPUs are identical)
     struct Grids {
         int lane, tile, solo;

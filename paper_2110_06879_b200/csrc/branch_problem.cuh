@@ -37,12 +37,7 @@ enum Field : int {
     F_RHO = 32,   // 8 penalties
     F_LTIJ = 40, F_LTJI = 41, F_RHOT = 42,
     F_VMIN_I = 43, F_VMAX_I = 44, F_VMIN_J = 45, F_VMAX_J = 46, F_R2 = 47,
-    kFields = 48,
-    F_H = 48,            // lane phase: the TRON Hessian, 36 fields (HessSmem);
-                         // tile / solo phases: the cached Hessian (kGhCache)
-    kFieldsHess = 84,
-    F_GC = 84,           // tile / solo phases: the cached gradient, 6 fields
-    kFieldsCache = 90
+    kFields = 48
 };
 
 // One branch's data: field f of slot s lives at smem[f * S + s].
@@ -163,23 +158,11 @@ struct YcView {
 };
 
 // The branch subproblem over a shared-memory slot (kernels.cpp:17-163).
-// kHessSmem: the TRON Hessian lives in the slot's F_H fields (lane phase).
-template <int N, int S, bool kHessSmem = false, bool kCache = false>
+template <int N, int S>
 struct BranchProb {
     static constexpr bool kLimited = N == 6;
-    static constexpr bool kGhCache = kCache;  // gradient / Hessian kept across rejected steps
-    __device__ __forceinline__ double cache_g(int i) const { return s(F_GC + i); }
-    __device__ __forceinline__ double cache_h(int k) const { return s(F_H + k); }
-    __device__ __forceinline__ void cache_put_g(int i, double v) const { s.set(F_GC + i, v); }
-    __device__ __forceinline__ void cache_put_h(int k, double v) const { s.set(F_H + k, v); }
     Slot<S> s;
     mutable double cc_, ss_;  // sincos at the last gradient point
-
-    template <int NN>
-    __device__ __forceinline__ auto hess_store() const {
-        if constexpr (kHessSmem) return HessSmem<S>{s.p + F_H * S};
-        else return HessRegs<NN>{};
-    }
 
     __device__ __forceinline__ double lo(int i) const {
         switch (i) {
@@ -312,95 +295,6 @@ struct BranchProb {
                 }
             }
         }
-    }
-
-    // One Hessian entry (i, j) with exactly the operation sequence
-    // eval<false, false, true> applies to h[i * N + j] (the flow terms, the
-    // w rows, the angle rows, then the two line-limit passes), for lanes of a
-    // tile that split the Hessian among them (TileSearch::hessian).  Uses the
-    // sincos of the last gradient() call, like hessian().
-    __device__ __forceinline__ double hess_entry(const double* x, int i, int j) const {
-        const Basis b = make_basis(x[0], x[1], cc_, ss_);
-        const YcView<S> yc{s};
-        const double ca[4] = {yc(0), -yc(1), yc(6), -yc(7)};
-        const double cb[4] = {yc(2), -yc(3), yc(4), -yc(5)};
-        const double cc[4] = {yc(3), yc(2), -yc(5), -yc(4)};
-        const double wi_v = b.vi * b.vi, wj_v = b.vj * b.vj;
-        const double wr_v = b.vivj * b.c, wim_v = b.vivj * b.s;
-        auto fv = [&](int k) {
-            const double av = k < 2 ? wi_v : wj_v;
-            return ca[k] * av + cb[k] * wr_v + cc[k] * wim_v;
-        };
-        auto fg = [&](int k, int q) {
-            const int a = k < 2 ? 0 : 1;
-            const double ag = a == 0 ? 2 * b.vi : 2 * b.vj;
-            if (q == a) return ca[k] * ag + cb[k] * wr_g(b, q) + cc[k] * wim_g(b, q);
-            return cb[k] * wr_g(b, q) + cc[k] * wim_g(b, q);
-        };
-        auto fh = [&](int k, int p, int q) {
-            const int a = k < 2 ? 0 : 1;
-            if (p == a && q == a) return ca[k] * 2.0;
-            return cb[k] * wr_h(b, p, q) + cc[k] * wim_h(b, p, q);
-        };
-        double acc = 0.0;
-        if (i < 4 && j < 4) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const double rh = s(F_RHO + k), yv = s(F_Y + k);
-                const double d = fv(k) - s(F_TGT + k) + s(F_Z + k);
-                const double w = yv + rh * d;
-                const double gg = rh * fg(k, i) * fg(k, j);
-                if (flow_h_zero(k, i, j)) acc += gg;
-                else acc += w * fh(k, i, j) + gg;
-            }
-#pragma unroll
-            for (int t = 0; t < 2; ++t) {
-                const int row = t == 0 ? 4 : 6;
-                const int a = t;
-                if (i == a && j == a) {
-                    const double v = x[a];
-                    const double ev = v * v;
-                    const double eg = 2 * v;
-                    const double rh = s(F_RHO + row), yv = s(F_Y + row);
-                    const double d = ev - s(F_TGT + row) + s(F_Z + row);
-                    const double w = yv + rh * d;
-                    acc += w * 2.0 + rh * eg * eg;
-                }
-            }
-            if (i == 2 && j == 2) acc += s(F_RHO + 5);
-            if (i == 3 && j == 3) acc += s(F_RHO + 7);
-        }
-        if constexpr (kLimited) {
-            const double rho_t = s(F_RHOT);
-#pragma unroll
-            for (int t = 0; t < 2; ++t) {
-                const int kp = t == 0 ? 0 : 2, kq = kp + 1;
-                const int srow = 4 + t;
-                const double lt = s(t == 0 ? F_LTIJ : F_LTJI);
-                const double pv = fv(kp), qv = fv(kq);
-                const double res = pv * pv + qv * qv + x[srow];
-                const double w = lt + rho_t * res;
-                auto gr = [&](int q) { return 2 * pv * fg(kp, q) + 2 * qv * fg(kq, q); };
-                if (i < 4 && j < 4) {
-                    const double w2 = w * 2.0;
-                    double a2;
-                    if (flow_h_zero(kp, i, j))
-                        a2 = fg(kp, i) * fg(kp, j) + fg(kq, i) * fg(kq, j);
-                    else
-                        a2 = fg(kp, i) * fg(kp, j) + pv * fh(kp, i, j) + fg(kq, i) * fg(kq, j) +
-                             qv * fh(kq, i, j);
-                    acc += w2 * a2;
-                    acc += rho_t * gr(i) * gr(j);
-                } else if (i < 4 && j == srow) {
-                    acc += rho_t * gr(i) * 1.0;
-                } else if (i == srow && j < 4) {
-                    acc += rho_t * 1.0 * gr(j);
-                } else if (i == srow && j == srow) {
-                    acc += rho_t * 1.0 * 1.0;
-                }
-            }
-        }
-        return acc;
     }
 
     __device__ __forceinline__ double value(const double* x) const {

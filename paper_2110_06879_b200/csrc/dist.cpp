@@ -80,7 +80,7 @@ public:
              const unsigned char* id)
         : net_(net), cfg_(cfg), rank_(rank), world_(world) {
         part_ = partition_buses(net, world);
-        plan_ = make_plan(net, part_, rank);
+        plan_ = make_plan(net, part_, rank, world);
         sess_ = std::make_unique<Session>(net, cfg, world > 1 ? &plan_ : nullptr);
         ncclUniqueId uid;
         std::memcpy(uid.internal, id, sizeof uid.internal);

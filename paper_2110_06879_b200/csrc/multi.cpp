@@ -38,7 +38,7 @@ public:
         for (int p = 0; p < k; ++p) {
             SolverConfig c = cfg;
             c.device = cfg.device + (p % ndev);
-            plans_.push_back(make_plan(net, part_of_bus_, p));
+            plans_.push_back(make_plan(net, part_of_bus_, p, k));
             parts_.push_back(std::make_unique<Session>(net, c, &plans_.back()));
         }
         // peer access between distinct devices (NVLink)

@@ -17,7 +17,11 @@ std::vector<int> partition_buses(const Network& net, int k) {
         const int f = net.lines[b].from, t = net.lines[b].to;
         adj[f].push_back(t);
         adj[t].push_back(f);
-        weight[f] += 4;  // branch solved on the from-bus part (the dominant work)
+        // a branch is solved on its from-bus part (the dominant work); a
+        // rate-limited branch (6 variables + the AL loop) costs about twice
+        // an unlimited one per TRON iteration (census) and runs
+        // the AL tails, so it weighs double
+        weight[f] += net.lines[b].limited() ? 8 : 4;
     }
     for (auto& a : adj) std::sort(a.begin(), a.end());
     std::vector<int> order;
@@ -50,9 +54,10 @@ std::vector<int> partition_buses(const Network& net, int k) {
     return part;
 }
 
-PartPlan make_plan(const Network& net, const std::vector<int>& part, int p) {
+PartPlan make_plan(const Network& net, const std::vector<int>& part, int p, int k) {
     PartPlan pl;
-    const int k = part.empty() ? 1 : 1 + *std::max_element(part.begin(), part.end());
+    // k parts as requested, whether or not the partition left some empty
+    k = std::max({k, 1, part.empty() ? 1 : 1 + *std::max_element(part.begin(), part.end())});
     pl.part = p;
     pl.parts = k;
     pl.send_x.assign(k, {});

@@ -31,10 +31,12 @@ struct PartPlan {
 };
 
 // part[i] for every bus: BFS order from bus 0 over the branch graph (ties by
-// index), cut into k contiguous chunks balancing owned branches.
+// index), cut into k contiguous chunks balancing owned branch work.  Parts
+// may be empty when k exceeds what the graph can fill.
 std::vector<int> partition_buses(const Network& net, int k);
 
-PartPlan make_plan(const Network& net, const std::vector<int>& part, int p);
+// Plan of part p of k (send_x / recv_x sized k, whatever parts are empty).
+PartPlan make_plan(const Network& net, const std::vector<int>& part, int p, int k);
 
 }  // namespace ga
 

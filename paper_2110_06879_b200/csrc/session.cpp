@@ -96,6 +96,7 @@ Session::Session(const Network& net, const SolverConfig& cfg, const PartPlan* pl
 Session::~Session() { free_all(); }
 
 void Session::free_all() {
+    cudaSetDevice(cfg_.device);  // no throw: runs in the destructor
     if (stream_) cudaStreamSynchronize(stream_);
     for (void* p : allocs_) cudaFreeAsync(p, stream_);  // back to the device pool
     if (!allocs_.empty() && stream_) cudaStreamSynchronize(stream_);
@@ -257,6 +258,7 @@ void Session::cold_start() {
 }
 
 void Session::upload_state(const HostState& s) {
+    use_device();
     const size_t nl = static_cast<size_t>(dn_.nl);
     auto put = [&](double* dst, const std::vector<double>& v) {
         if (!v.empty())
@@ -282,6 +284,7 @@ void Session::upload_state(const HostState& s) {
 }
 
 void Session::download_state(HostState& s) const {
+    use_device();
     const int m = dn_.m, nb = dn_.nb;
     const size_t nl = static_cast<size_t>(dn_.nl);
     auto get = [&](std::vector<double>& v, const double* src, size_t n) {
@@ -304,6 +307,7 @@ void Session::download_state(HostState& s) const {
 
 void Session::download_solution_inputs(std::vector<double>& gen_rows, std::vector<double>& w,
                                        std::vector<double>& th) const {
+    use_device();
     gen_rows.resize(2 * static_cast<size_t>(dn_.ng));
     w.resize(dn_.nb);
     th.resize(dn_.nb);
@@ -320,6 +324,7 @@ void Session::download_solution_inputs(std::vector<double>& gen_rows, std::vecto
 }
 
 void Session::set_loads(const std::vector<double>& pd, const std::vector<double>& qd) {
+    use_device();
     check(cudaMemcpyAsync(dn_.b_pd, pd.data(), pd.size() * sizeof(double), cudaMemcpyHostToDevice,
                           stream_), "set_loads");
     check(cudaMemcpyAsync(dn_.b_qd, qd.data(), qd.size() * sizeof(double), cudaMemcpyHostToDevice,
@@ -334,6 +339,7 @@ void Session::set_loads(const std::vector<double>& pd, const std::vector<double>
 }
 
 void Session::set_gen_p_bounds(const std::vector<double>& pmin, const std::vector<double>& pmax) {
+    use_device();
     check(cudaMemcpyAsync(dn_.g_pmin, pmin.data(), pmin.size() * sizeof(double),
                           cudaMemcpyHostToDevice, stream_), "set_gen_p_bounds");
     check(cudaMemcpyAsync(dn_.g_pmax, pmax.data(), pmax.size() * sizeof(double),
@@ -346,6 +352,7 @@ void Session::set_gen_p_bounds(const std::vector<double>& pmin, const std::vecto
 }
 
 void Session::clamp_gen_p() {
+    use_device();
     launch_clamp_gen_p(dn_, ds_, stream_);
     check(cudaGetLastError(), "clamp_gen_p");
 }
@@ -380,6 +387,7 @@ BranchCfg branch_cfg(const SolverConfig& c) {
 }
 
 long Session::run_phase(int phase, double z_inf, double prev_z_inf) {
+    use_device();
     long ret = 0;
     launch_reset_scalars(sc_, stream_);
     switch (phase) {
@@ -405,6 +413,7 @@ long Session::run_phase(int phase, double z_inf, double prev_z_inf) {
 }
 
 int Session::timed_steps(int k, size_t flush_bytes, double* step_ms, double* records) {
+    use_device();
     if (flush_bytes > flush_size_) {
         if (flush_buf_) cudaFree(flush_buf_);
         flush_buf_ = nullptr;
@@ -504,10 +513,12 @@ void Session::enqueue_xbar_zy_phase(bool copy_scalars) {
 }
 
 void Session::enqueue_scalars_d2h() {
+    use_device();
     check(cudaMemcpyAsync(sc_host_, sc_, sizeof(DevScalars), cudaMemcpyDeviceToHost, stream_), "D2H");
 }
 
 IterScalars Session::read_scalars() {
+    use_device();
     check(cudaStreamSynchronize(stream_), "iteration sync");
     const DevScalars& h = *sc_host_;
     IterScalars r;
@@ -527,6 +538,7 @@ void Session::outer_update() {
 }
 
 double Session::rho_max() {
+    use_device();
     launch_rowmax(ds_.rho, dn_.m, red_, stream_);
     unsigned long long bits = 0;
     check(cudaMemcpyAsync(&bits, red_, sizeof bits, cudaMemcpyDeviceToHost, stream_), "D2H");
@@ -535,18 +547,21 @@ double Session::rho_max() {
 }
 
 long long Session::tron_iterations() const {
+    use_device();
     DevScalars h;
     check(cudaMemcpy(&h, sc_, sizeof h, cudaMemcpyDeviceToHost), "D2H");
     return static_cast<long long>(h.tron_iters4);
 }
 
 long long Session::sincos_calls() const {
+    use_device();
     DevScalars h;
     check(cudaMemcpy(&h, sc_, sizeof h, cudaMemcpyDeviceToHost), "D2H");
     return static_cast<long long>(h.tron_iters6);
 }
 
 void Session::step_counters(long long out[4]) const {
+    use_device();
     DevScalars h;
     check(cudaMemcpy(&h, sc_, sizeof h, cudaMemcpyDeviceToHost), "D2H");
     out[0] = static_cast<long long>(h.tron_iters4);
@@ -556,10 +571,18 @@ void Session::step_counters(long long out[4]) const {
 }
 
 void Session::branch_costs(int* out) const {
+    use_device();
     if (dn_.nl)
         check(cudaMemcpy(out, ds_.br_cost, dn_.nl * sizeof(int), cudaMemcpyDeviceToHost), "D2H");
 }
 
-void Session::sync() const { check(cudaStreamSynchronize(stream_), "sync"); }
+void Session::sync() const {
+    use_device();
+    check(cudaStreamSynchronize(stream_), "sync");
+}
+
+// Every method that touches device memory or the stream makes the session's
+// GPU current first: sessions on different GPUs may share a host thread.
+void Session::use_device() const { check(cudaSetDevice(cfg_.device), "cudaSetDevice"); }
 
 }  // namespace ga

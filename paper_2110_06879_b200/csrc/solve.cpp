@@ -1,7 +1,6 @@
 // solve.cpp — Algorithm-1 loop control over a device-resident Session
-// (proj/src/driver.cpp:65-246), warm-start tracking
-// (proj/src/tracking.cpp:30-196) and the report writers
-// (proj/src/outputs.cpp).
+// (proj/src/driver.cpp:65-246) and warm-start tracking
+// (proj/src/tracking.cpp:30-85); file formats are in io.cpp.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -10,8 +9,6 @@
 #include <map>
 #include <memory>
 #include <sstream>
-
-#include <json.hpp>
 
 #include "ga_math.h"
 #include "solver.hpp"
@@ -244,175 +241,6 @@ std::vector<PeriodReport> run_tracking(const Network& net, const SolverConfig& c
         reports.push_back(std::move(pr));
     }
     return reports;
-}
-
-// tracking.cpp:114-196
-TrackingScenario load_profile_csv(const std::string& path, const Network& net) {
-    std::ifstream in(path);
-    if (!in) throw ParseError("cannot open profile file: " + path);
-    std::string line;
-    if (!std::getline(in, line)) throw ParseError("empty profile file: " + path);
-    auto split = [](const std::string& s) {
-        std::vector<std::string> out;
-        std::stringstream ss(s);
-        std::string f;
-        while (std::getline(ss, f, ',')) {
-            f.erase(0, f.find_first_not_of(" \t\r"));
-            f.erase(f.find_last_not_of(" \t\r") + 1);
-            out.push_back(f);
-        }
-        return out;
-    };
-    const auto header = split(line);
-    bool per_bus_mode;
-    if (header.size() == 2 && header[0] == "period" && header[1] == "multiplier") per_bus_mode = false;
-    else if (header.size() == 3 && header[0] == "period" && header[1] == "bus" &&
-             header[2] == "multiplier")
-        per_bus_mode = true;
-    else throw ParseError("unrecognized profile header: " + line);
-
-    std::map<int, double> uniform;
-    std::map<int, std::vector<double>> table;
-    int lineno = 1;
-    while (std::getline(in, line)) {
-        ++lineno;
-        const auto fields = split(line);
-        if (fields.empty() || (fields.size() == 1 && fields[0].empty())) continue;
-        try {
-            if (!per_bus_mode) {
-                if (fields.size() != 2) throw std::invalid_argument("field count");
-                uniform[std::stoi(fields[0])] = std::stod(fields[1]);
-            } else {
-                if (fields.size() != 3) throw std::invalid_argument("field count");
-                const int period = std::stoi(fields[0]);
-                const int bus = std::stoi(fields[1]);
-                const auto it = net.bus_index.find(bus);
-                if (it == net.bus_index.end())
-                    throw std::invalid_argument("unknown bus " + std::to_string(bus));
-                auto& row = table[period];
-                row.resize(net.buses.size(), 1.0);
-                row[it->second] = std::stod(fields[2]);
-            }
-        } catch (const std::exception& e) {
-            throw ParseError("profile line " + std::to_string(lineno) + ": " + e.what());
-        }
-    }
-    std::map<int, double> keys;
-    if (per_bus_mode)
-        for (const auto& kv : table) keys[kv.first] = 1.0;
-    else keys = uniform;
-    if (keys.empty()) throw ParseError("profile has no data rows: " + path);
-    const int periods = static_cast<int>(keys.size());
-    for (int t = 1; t <= periods; ++t)
-        if (!keys.count(t))
-            throw ParseError("profile periods must be contiguous 1..T; missing " + std::to_string(t));
-    TrackingScenario sc;
-    sc.multipliers.assign(periods, 1.0);
-    if (per_bus_mode) {
-        sc.per_bus.resize(periods);
-        for (auto& kv : table) sc.per_bus[kv.first - 1] = std::move(kv.second);
-    } else {
-        for (const auto& kv : uniform) sc.multipliers[kv.first - 1] = kv.second;
-    }
-    return sc;
-}
-
-// ---- outputs (outputs.cpp) ----------------------------------------------
-namespace {
-
-const char* status_name(SolveStatus s) {
-    switch (s) {
-        case SolveStatus::Converged: return "converged";
-        case SolveStatus::IterationLimit: return "iteration_limit";
-        case SolveStatus::Diverged: return "diverged";
-    }
-    return "unknown";
-}
-
-std::ofstream open_or_throw(const std::string& path) {
-    std::ofstream out(path);
-    if (!out) throw std::runtime_error("cannot write output file: " + path);
-    return out;
-}
-
-std::string fmt17(double v) {
-    char buf[32];
-    std::snprintf(buf, sizeof buf, "%.17g", v);
-    return buf;
-}
-
-}  // namespace
-
-double report_gap(double objective, double reference) {
-    if (!(reference > 0.0)) throw std::invalid_argument("reference objective must be positive");
-    return std::abs(objective - reference) / reference;
-}
-
-void write_solution_json(const std::string& path, const Network& net, const SolveReport& r,
-                         double ref_objective) {
-    nlohmann::json j;
-    j["status"] = status_name(r.status);
-    j["outer_iterations"] = r.outer_iterations;
-    j["inner_iterations"] = r.inner_iterations;
-    j["branch_solve_failures"] = r.branch_solve_failures;
-    if (!r.diagnostic.empty()) j["diagnostic"] = r.diagnostic;
-    j["metrics"] = {{"objective", r.quality.objective},
-                    {"balance_inf", r.quality.balance_inf},
-                    {"limit_violation", r.quality.limit_violation},
-                    {"bound_violation", r.quality.bound_violation},
-                    {"c_inf", r.quality.c_inf}};
-    if (ref_objective > 0.0) {
-        j["metrics"]["reference_objective"] = ref_objective;
-        j["metrics"]["gap"] = report_gap(r.quality.objective, ref_objective);
-    }
-    j["phase_times_s"] = {{"x", r.phase_times.x_s},
-                          {"xbar", r.phase_times.xbar_s},
-                          {"z", r.phase_times.z_s},
-                          {"y", r.phase_times.y_s}};
-    auto gens = nlohmann::json::array();
-    for (size_t g = 0; g < r.solution.pg.size(); ++g)
-        gens.push_back({{"bus", net.buses[net.gens[g].bus].id},
-                        {"pg", r.solution.pg[g]},
-                        {"qg", r.solution.qg[g]}});
-    j["generators"] = gens;
-    auto buses = nlohmann::json::array();
-    for (size_t i = 0; i < r.solution.vm.size(); ++i)
-        buses.push_back({{"bus", net.buses[i].id}, {"vm", r.solution.vm[i]}, {"va", r.solution.va[i]}});
-    j["buses"] = buses;
-    auto branches = nlohmann::json::array();
-    for (size_t b = 0; b < net.lines.size(); ++b) {
-        const Line& l = net.lines[b];
-        const double* f = &r.solution.flows[4 * b];
-        branches.push_back({{"from", net.buses[l.from].id},
-                            {"to", net.buses[l.to].id},
-                            {"pij", f[0]},
-                            {"qij", f[1]},
-                            {"pji", f[2]},
-                            {"qji", f[3]}});
-    }
-    j["branches"] = branches;
-    open_or_throw(path) << j.dump(2) << "\n";
-}
-
-void write_convergence_csv(const std::string& path, const std::vector<IterationRecord>& s) {
-    std::ofstream out = open_or_throw(path);
-    out << "outer,inner,primal_res,dual_res,z_norm,elapsed_s\n";
-    for (const auto& r : s)
-        out << r.outer << ',' << r.inner << ',' << fmt17(r.primal_res) << ',' << fmt17(r.dual_res)
-            << ',' << fmt17(r.z_norm) << ',' << fmt17(r.elapsed_s) << '\n';
-}
-
-void write_periods_csv(const std::string& path, const std::vector<PeriodReport>& p,
-                       const std::vector<double>& refs) {
-    std::ofstream out = open_or_throw(path);
-    out << "period,inner_iters,time_s,viol_inf,gap\n";
-    for (size_t t = 0; t < p.size(); ++t) {
-        out << p[t].period << ',' << p[t].report.inner_iterations << ',' << fmt17(p[t].time_s) << ','
-            << fmt17(p[t].report.quality.c_inf) << ',';
-        if (t < refs.size() && refs[t] > 0.0) out << fmt17(report_gap(p[t].report.quality.objective, refs[t]));
-        else out << "nan";
-        out << '\n';
-    }
 }
 
 }  // namespace ga

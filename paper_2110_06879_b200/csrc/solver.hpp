@@ -209,6 +209,7 @@ public:
                                   std::vector<double>& th) const override;
 
 private:
+    void use_device() const;
     void upload_network();
     void free_all();
     Network net_;

@@ -392,11 +392,6 @@ struct TronState {
     double f;
     double delta;
     int iter;
-    // x (and the problem data) unchanged since the gradient / Hessian were
-    // last computed, i.e. the last step was rejected: with a problem that
-    // keeps a copy (P::kGhCache) they are reloaded instead of recomputed —
-    // the same bits, since the evaluation is deterministic.
-    bool ghc;
 };
 
 // Starts a solve: clip x into the box and evaluate f (tron.cpp:235-240).
@@ -408,29 +403,10 @@ GA_FN bool tron_begin(const P& prob, TronState<N>& st) {
     st.f = prob.value(st.x);
     st.delta = 0.0;
     st.iter = 0;
-    st.ghc = false;
     return sfinite(st.f);
 }
 
 enum TronStep : int { kStepContinue = 0, kStepConverged = 1, kStepError = 2, kStepExhausted = 3 };
-
-// Hessian storage of one solve: registers (HessRegs) or a strided column of
-// shared memory (HessSmem, the lane phase: frees 72 registers per thread for
-// occupancy / batched trials).  Both are read as h[i * N + j].
-template <int N>
-struct HessRegs {
-    double v[N * N];
-    GA_FN double operator[](int k) const { return v[k]; }
-    GA_FN void put(int k, double x) { v[k] = x; }
-};
-#if defined(__CUDACC__)
-template <int S>
-struct HessSmem {
-    double* p;  // element k at p[k * S]
-    __device__ __forceinline__ double operator[](int k) const { return p[k * S]; }
-    __device__ __forceinline__ void put(int k, double x) const { p[k * S] = x; }
-};
-#endif
 
 // Sequential search strategy (one thread per solve): the reference's loops.
 struct SerialSearch {
@@ -477,31 +453,11 @@ struct SerialSearch {
 // computed exactly as the sequential loop computes it (scaling by powers of
 // two is exact), so the selected step is bit-identical.
 template <int T>
-#ifndef GA_TILE_HESS
-#define GA_TILE_HESS 0  // measured slower
-#endif
 struct TileSearch {
     static constexpr bool kClocked = T == 32;
     static constexpr bool kOolDivSqrt = false;
-    // The tile's lanes split the N*N Hessian entries (each computed with the
-    // serial evaluation's exact operation sequence, P::hess_entry) and
-    // exchange them with shuffles: every lane ends with the full matrix.
     template <int N, class P>
-    __device__ void hessian(const P& prob, const double* x, double* h) const {
-        if constexpr (!GA_TILE_HESS) {
-            prob.hessian(x, h);
-        } else {
-            constexpr int E = N * N, M = (E + T - 1) / T;
-            double mine[M];
-#pragma unroll
-            for (int m = 0; m < M; ++m) {
-                const int e = rank + m * T;
-                mine[m] = e < E ? prob.hess_entry(x, e / N, e % N) : 0.0;
-            }
-#pragma unroll
-            for (int e = 0; e < E; ++e) h[e] = __shfl_sync(mask, mine[e / T], e % T, T);
-        }
-    }
+    __device__ void hessian(const P& prob, const double* x, double* h) const { prob.hessian(x, h); }
     unsigned mask;  // warp lanes of this tile
     int base;       // first warp lane of the tile
     int rank;       // lane within the tile
@@ -625,41 +581,18 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
 #pragma unroll
     for (int i = 0; i < N; ++i) { l[i] = prob.lo(i); u[i] = prob.hi(i); }
     GA_CLK_DECL
-    constexpr bool kCache = P::kGhCache;
-    const bool cached = kCache && st.ghc;
     double g[N];
-    if (cached) {
-#pragma unroll
-        for (int i = 0; i < N; ++i) g[i] = prob.cache_g(i);
-    } else {
-        prob.gradient(st.x, g);
-    }
+    prob.gradient(st.x, g);
 #pragma unroll
     for (int i = 0; i < N; ++i)
         if (!sfinite(g[i])) return kStepError;
     if (proj_grad_norm<N>(st.x, g, l, u) <= cfg.gtol) return kStepConverged;
     GA_CLK(0);
-    auto h = prob.template hess_store<N>();
-    {
-        double hr[N * N];
-        if (cached) {
+    double h[N * N];
+    search.template hessian<N>(prob, st.x, h);
 #pragma unroll
-            for (int i = 0; i < N * N; ++i) hr[i] = prob.cache_h(i);
-        } else {
-            search.template hessian<N>(prob, st.x, hr);
-#pragma unroll
-            for (int i = 0; i < N * N; ++i)
-                if (!sfinite(hr[i])) return kStepError;
-            if constexpr (kCache) {
-#pragma unroll
-                for (int i = 0; i < N; ++i) prob.cache_put_g(i, g[i]);
-#pragma unroll
-                for (int i = 0; i < N * N; ++i) prob.cache_put_h(i, hr[i]);
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < N * N; ++i) h.put(i, hr[i]);
-    }
+    for (int i = 0; i < N * N; ++i)
+        if (!sfinite(h[i])) return kStepError;
     constexpr bool kOol = Search::kOolDivSqrt;
     if (st.iter == 0 && st.delta == 0.0) st.delta = smax(vnorm2<N, kOol>(g), cfg.delta_floor);
 
@@ -690,7 +623,6 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
     if (ratio < 0.25) st.delta = 0.25 * smax(snorm, 1e-12);
     else if (ratio > 0.75 && snorm >= 0.9 * st.delta) st.delta = smin(2.0 * st.delta, kTronDeltaMax);
     const bool accepted = ared > 0.0 && ratio > kTronEta;
-    st.ghc = !accepted;
     if (accepted) {
 #pragma unroll
         for (int i = 0; i < N; ++i) st.x[i] = xt[i];

@@ -105,6 +105,15 @@ gridadmm_status gridadmm_session_get_state(const gridadmm_session* s,
 gridadmm_status gridadmm_session_set_state(gridadmm_session* s,
                                            const gridadmm_state_view* v);
 
+/* The reference's solve(net, cfg, initial, final) (proj/src/driver.cpp:140-246)
+ * on the session's device state: Algorithm 1 with cfg's stop rules, starting
+ * from the current state (warm != 0, the `initial` argument) or from a fresh
+ * cold start (warm == 0).  The state after the solve stays on the device
+ * (the `final_state` argument: read it with gridadmm_session_get_state).
+ * Status and report semantics are those of gridadmm_solve. */
+gridadmm_status gridadmm_session_solve(gridadmm_session* s, const gridadmm_config* cfg,
+                                       int warm, gridadmm_report** out);
+
 /* Runs one phase on the device state.  For GRIDADMM_PHASE_BRANCHES,
  * *aux receives the number of branch solve failures; for BUSES, *aux is -1
  * or the internal index of the first singular bus; for OUTER, aux[0] is

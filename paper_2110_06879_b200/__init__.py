@@ -81,6 +81,7 @@ EXT_SYMBOLS = {
     "gridadmm_network_partition": (_I, [_P, _I, _IP]),
     "gridadmm_session_new": (_I, [_P, _P, ctypes.POINTER(_P)]),
     "gridadmm_session_free": (None, [_P]),
+    "gridadmm_session_solve": (_I, [_P, _P, _I, ctypes.POINTER(_P)]),
     "gridadmm_nccl_unique_id": (_I, [ctypes.c_char_p]),
     "gridadmm_session_new_dist": (_I, [_P, _P, _I, _I, ctypes.c_char_p, ctypes.POINTER(_P)]),
     "gridadmm_session_get_state": (_I, [_P, ctypes.POINTER(StateView)]),
@@ -376,6 +377,7 @@ class Session:
         if _handle is None:
             _check(lib().gridadmm_session_new(net.handle, cfg.handle, ctypes.byref(h)))
         self._h = h
+        self._dims = (net.num_generators, net.num_buses)
         self.shapes = state_shapes(net.num_buses, net.num_generators, net.num_branches)
 
     @classmethod
@@ -385,6 +387,15 @@ class Session:
         _check(lib().gridadmm_session_new_dist(net.handle, cfg.handle, rank, world, nccl_id,
                                                ctypes.byref(h)))
         return cls(net, cfg, _handle=h)
+
+    def solve(self, cfg: Config, warm: bool = True):
+        """Algorithm 1 on this session's device state (gridadmm_session_solve):
+        warm=True continues from the current state.  Returns (status, Report)."""
+        rep = _P()
+        st = lib().gridadmm_session_solve(self._h, cfg.handle, int(warm), ctypes.byref(rep))
+        if not rep:
+            _check(st)
+        return st, Report(rep, self._dims)
 
     def get_state(self) -> Dict[str, np.ndarray]:
         arrs = {k: np.zeros(n) for k, n in self.shapes.items()}

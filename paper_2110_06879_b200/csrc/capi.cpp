@@ -398,6 +398,22 @@ gridadmm_status gridadmm_session_new(const gridadmm_network* net, const gridadmm
 
 void gridadmm_session_free(gridadmm_session* s) { delete s; }
 
+gridadmm_status gridadmm_session_solve(gridadmm_session* s, const gridadmm_config* cfg, int warm,
+                                       gridadmm_report** out) {
+    if (!s || !cfg || !out) return fail(GRIDADMM_ERR_INVALID_ARG, "null argument to session_solve");
+    try {
+        auto* rep = new gridadmm_report{ga::solve(*s->e, cfg->solver, warm != 0), s->e->network()};
+        *out = rep;
+        const gridadmm_status st = status_of(rep->report.status);
+        if (st != GRIDADMM_OK)
+            g_last_error = rep->report.diagnostic.empty() ? "solve did not converge"
+                                                          : rep->report.diagnostic;
+        return st;
+    } catch (const std::exception& e) {
+        return fail(GRIDADMM_ERR_INTERNAL, e.what());
+    }
+}
+
 gridadmm_status gridadmm_nccl_unique_id(unsigned char* out) {
     if (!out) return fail(GRIDADMM_ERR_INVALID_ARG, "null argument to nccl_unique_id");
     return guarded([&]() -> gridadmm_status {

@@ -94,6 +94,21 @@ struct DevScalars {
     unsigned long long exec6;       // (6-var); < TRON iterations when fixed points are skipped
 };
 
+// Solution extraction + quality metrics of a finished solve (extract.cu).
+struct ExtractScalars {
+    unsigned long long balance_inf;      // max(|pbal|, |qbal|), bits
+    unsigned long long bound_violation;  // max(0, generator / voltage bound excess), bits
+    int n_cand;                          // branches on the line-limit candidate list
+    int pad;
+};
+struct DevExtract {
+    double* flows = nullptr;  // [4 * nl] AoS pij qij pji qji
+    double* vm = nullptr;     // [nb]
+    double* va = nullptr;     // [nb]
+    int* cand = nullptr;      // [nl] line-limit candidates (unordered)
+    ExtractScalars* sc = nullptr;
+};
+
 struct BranchCfg {
     double gtol = 1e-6;
     int max_iterations = 200;
@@ -109,6 +124,8 @@ struct BranchCfg {
 };
 
 // ---- launchers (kernels.cu / branch.cu) ----------------------------------
+// Solution voltages / flows and the order-free quality maxima (extract.cu).
+void launch_extract(const DevNet& n, const DevState& s, const DevExtract& e, cudaStream_t st);
 void launch_generators(const DevNet& n, const DevState& s, cudaStream_t st);
 // `mid` (optional) is recorded between the lane-phase and tile-phase kernels.
 void launch_branches(const DevNet& n, const DevState& s, const BranchCfg& cfg,

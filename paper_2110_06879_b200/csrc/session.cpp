@@ -225,6 +225,13 @@ void Session::upload_network() {
             alloc(d_recv_[q], plan_.recv_x[q].size()); put(d_recv_[q], plan_.recv_x[q]);
         }
     }
+    if (plan_.parts <= 1) {
+        alloc(ext_.flows, 4 * static_cast<size_t>(nl));
+        alloc(ext_.vm, nb);
+        alloc(ext_.va, nb);
+        alloc(ext_.cand, nl);
+        alloc(ext_.sc, 1);
+    }
     alloc(sc_, 1);
     alloc(red_, 1);
     size_t total = 0;
@@ -321,6 +328,39 @@ void Session::download_solution_inputs(std::vector<double>& gen_rows, std::vecto
                               cudaMemcpyDeviceToHost, stream_), "D2H");
     }
     check(cudaStreamSynchronize(stream_), "sync");
+}
+
+bool Session::extract_on_device(Solution& sol, QualityMetrics& q) {
+    if (plan_.parts > 1 || !ext_.sc) return false;
+    use_device();
+    const int ng = dn_.ng, nb = dn_.nb, nl = dn_.nl;
+    launch_extract(dn_, ds_, ext_, stream_);
+    check(cudaGetLastError(), "extract launch");
+    std::vector<double> gen_rows(2 * static_cast<size_t>(ng));
+    sol.vm.resize(nb);
+    sol.va.resize(nb);
+    sol.flows.resize(4 * static_cast<size_t>(nl));
+    ExtractScalars es{};
+    auto d2h = [&](void* dst, const void* src, size_t bytes) {
+        if (bytes) check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream_), "D2H");
+    };
+    d2h(gen_rows.data(), ds_.x, gen_rows.size() * sizeof(double));
+    d2h(sol.vm.data(), ext_.vm, nb * sizeof(double));
+    d2h(sol.va.data(), ext_.va, nb * sizeof(double));
+    d2h(sol.flows.data(), ext_.flows, sol.flows.size() * sizeof(double));
+    d2h(&es, ext_.sc, sizeof es);
+    check(cudaStreamSynchronize(stream_), "extract sync");
+    std::vector<int> cand(es.n_cand);
+    d2h(cand.data(), ext_.cand, cand.size() * sizeof(int));
+    check(cudaStreamSynchronize(stream_), "extract sync");
+    sol.pg.resize(ng);
+    sol.qg.resize(ng);
+    for (int g = 0; g < ng; ++g) {
+        sol.pg[g] = gen_rows[2 * static_cast<size_t>(g)];
+        sol.qg[g] = gen_rows[2 * static_cast<size_t>(g) + 1];
+    }
+    finish_metrics(net_, sol, cand, from_bits(es.balance_inf), from_bits(es.bound_violation), q);
+    return true;
 }
 
 void Session::set_loads(const std::vector<double>& pd, const std::vector<double>& qd) {

@@ -126,10 +126,38 @@ QualityMetrics evaluate_solution(const Network& net, const Solution& sol) {
     return q;
 }
 
+// The two metric pieces the device leaves to the host (extract.cu): the
+// objective, a sequential sum in generator order (driver.cpp:97-98), and the
+// line-limit violation with glibc's hypot over the candidate branches (any
+// other branch has hypot - rate < 0, driver.cpp:108-114).
+void finish_metrics(const Network& net, const Solution& sol, std::vector<int>& cand,
+                    double balance_inf, double bound_violation, QualityMetrics& q) {
+    q = QualityMetrics{};
+    for (int g = 0; g < net.ng(); ++g) {
+        const Gen& gen = net.gens[g];
+        q.objective += gen.c2 * sol.pg[g] * sol.pg[g] + gen.c1 * sol.pg[g] + gen.c0;
+    }
+    std::sort(cand.begin(), cand.end());
+    for (int b : cand) {
+        const Line& l = net.lines[b];
+        const double* f = &sol.flows[4 * static_cast<size_t>(b)];
+        q.limit_violation = max_list({q.limit_violation, std::hypot(f[0], f[1]) - l.rate,
+                                      std::hypot(f[2], f[3]) - l.rate});
+    }
+    q.limit_violation = smax(0.0, q.limit_violation);
+    q.balance_inf = balance_inf;
+    q.bound_violation = bound_violation;
+    q.c_inf = max_list({q.balance_inf, q.limit_violation, q.bound_violation});
+}
+
 namespace {
 
 void finish_report(Engine& s, SolveReport& rep) {
     trace_phase("iteration loop");
+    if (s.extract_on_device(rep.solution, rep.quality)) {
+        trace_phase("device extract + metrics");
+        return;
+    }
     std::vector<double> gen_rows, w, th;
     s.download_solution_inputs(gen_rows, w, th);
     trace_phase("solution download");

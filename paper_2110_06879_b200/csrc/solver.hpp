@@ -134,6 +134,9 @@ public:
     virtual double rho_max() = 0;
     virtual void download_solution_inputs(std::vector<double>& gen_rows, std::vector<double>& w,
                                           std::vector<double>& th) const = 0;
+    // Solution extraction + quality metrics on the device (extract.cu);
+    // false when this engine leaves them to the host (multi-part engines).
+    virtual bool extract_on_device(Solution& sol, QualityMetrics& q) { return false; }
     virtual int parts() const { return 1; }
     // k iterations each bracketed by CUDA events (see Session::timed_steps)
     virtual int timed_steps(int k, size_t flush_bytes, double* step_ms, double* records) = 0;
@@ -204,6 +207,7 @@ public:
     long long sincos_calls() const;
     void sync() const;
 
+    bool extract_on_device(Solution& sol, QualityMetrics& q) override;
     // Solution extraction inputs: x gen rows, bus_w, bus_theta.
     void download_solution_inputs(std::vector<double>& gen_rows, std::vector<double>& w,
                                   std::vector<double>& th) const override;
@@ -216,6 +220,7 @@ private:
     SolverConfig cfg_;
     DevNet dn_;
     DevState ds_;
+    DevExtract ext_;  // single-part sessions only
     DevScalars* sc_ = nullptr;       // device
     DevScalars* sc_host_ = nullptr;  // pinned mirror
     unsigned long long* red_ = nullptr;
@@ -247,6 +252,8 @@ std::unique_ptr<Engine> make_dist_engine(const Network& net, const SolverConfig&
 Solution extract_solution(const Network& net, const std::vector<double>& gen_rows,
                           const std::vector<double>& bus_w, const std::vector<double>& bus_theta);
 QualityMetrics evaluate_solution(const Network& net, const Solution& sol);
+void finish_metrics(const Network& net, const Solution& sol, std::vector<int>& cand,
+                    double balance_inf, double bound_violation, QualityMetrics& q);
 
 // ---- tracking (tracking.hpp) --------------------------------------------
 class RampError : public std::runtime_error {

@@ -213,3 +213,31 @@ def test_series_parity_synthetic_scale(gridadmm, oracle_mod, shape, lane_budget)
                              workers=os.cpu_count() or 1)
     assert len(rec) == len(series) == iters
     assert_bits_equal(rec[:, 0:3], series[:, 2:5], f"{shape} residuals")
+
+
+@pytest.mark.parametrize("shape,preset", [("case_ACTIVSg70k", "case_ACTIVSg70k"),
+                                          ("case_ACTIVSg25k", "case_ACTIVSg25k"),
+                                          ("case9241pegase", "case9241pegase")])
+def test_series_parity_headline_scale(gridadmm, oracle_mod, shape, preset):
+    """North-star bar at the BASELINE configs' own scale and penalties: the
+    first 100 inner iterations of the cold start (preset rho, default
+    tolerances) -- residual series and the whole final state bit for bit."""
+    from gridcases import synth
+    import os
+    iters = 100
+    path = synth.ensure_case(shape, "/tmp/gridadmm_cases")
+    net = gridadmm.Network(path)
+    rpq, rva = oracle_mod.ref_preset(preset)
+    cfg = gridadmm.Config(preset)
+    assert (cfg["rho_pq"], cfg["rho_va"]) == (rpq, rva)
+    sess = gridadmm.Session(net, cfg)
+    rec, _ = sess.iterate(iters)
+    ref = oracle_mod.RefNet(path)
+    series, _, fin = ref.solve(rho_pq=rpq, rho_va=rva, max_outer=1, max_inner=iters,
+                               workers=os.cpu_count() or 1)
+    assert len(rec) == len(series) == iters
+    assert_bits_equal(rec[:, 0:3], series[:, 2:5], f"{shape} residuals")
+    z_last = float(rec[-1, 2])
+    if not z_last <= 1e-4:
+        sess.phase("outer", z_last, -1.0)
+    assert_state_equal(sess.get_state(), fin, f"{shape} state after {iters} iterations")

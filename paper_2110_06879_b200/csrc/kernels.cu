@@ -69,6 +69,19 @@ __global__ void __launch_bounds__(kBlock) gen_kernel(DevNet n, DevState s) {
     reinterpret_cast<double2*>(s.x)[g] = out;
 }
 
+// The generator projection of one generator row (the expressions of
+// gen_kernel above), evaluated where the bus kernel consumes the row.
+__device__ __forceinline__ double gen_row_x(const DevNet& n, int row, double xb, double z, double y,
+                                            double rho) {
+    const int g = row >> 1;
+    if ((row & 1) == 0) {
+        const double p = (rho * (xb - z) - y - __ldg(n.g_c1 + g)) / (2.0 * __ldg(n.g_c2 + g) + rho);
+        return sclamp(p, __ldg(n.g_pmin + g), __ldg(n.g_pmax + g));
+    }
+    const double q = (rho * (xb - z) - y) / rho;
+    return sclamp(q, __ldg(n.g_qmin + g), __ldg(n.g_qmax + g));
+}
+
 // ---- buses (kernels.cpp:294-413) ----------------------------------------
 // Per bus, variables: [0] w, [1] theta, then one duplicate per row in gen_p,
 // gen_q, flow_p, flow_q order.  A's entries are implied by the group of each
@@ -156,6 +169,12 @@ __device__ __forceinline__ bool ge_solve(double* S, double* rhs, double* mu) {
 // Fusing z / y is exact: every row is consumed by exactly one bus
 // (proj/tests/test_decomp.cpp:59-71) and z / y of a row depend only on that
 // row, so the order "all buses, then all z, then all y" is not observable.
+// The iteration form (kZY) also absorbs the generator projection
+// (kernels.cpp:194-209): x of a generator row depends only on that row's
+// previous xbar, z, y, rho, which nothing between the generator phase and
+// the bus phase writes (the branch phase touches branch rows only), so it is
+// computed here — in the gather, the solve's unstaged reads and the write,
+// always from the same inputs, hence the same bits — and written once.
 #ifndef GA_BUS_BLOCK
 #define GA_BUS_BLOCK 128
 #endif
@@ -272,9 +291,12 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
         for (int u = 0; u < kUnroll; ++u) {
             if (row[u] >= 0) {
                 q[u] = __ldg(s.rho + row[u]);
-                xv[u] = __ldg(s.x + row[u]);
                 zv[u] = __ldg(s.z + row[u]);
                 yv[u] = __ldg(s.y + row[u]);
+                if (kZY && (g[u] == 2 || g[u] == 3))
+                    xv[u] = gen_row_x(n, row[u], __ldg(s.xbar + row[u]), zv[u], yv[u], q[u]);
+                else
+                    xv[u] = __ldg(s.x + row[u]);
             }
         }
 #pragma unroll
@@ -305,7 +327,10 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
         auto raw = [&](int k, double* q, double* c) {
             const int row = rows[k];
             *q = s.rho[row];
-            *c = *q * (s.x[row] + s.z[row]) + s.y[row];
+            const double xr = (kZY && k >= gl[2] && k < gl[4])
+                                  ? gen_row_x(n, row, s.xbar[row], s.z[row], s.y[row], *q)
+                                  : s.x[row];
+            *c = *q * (xr + s.z[row]) + s.y[row];
         };
         auto staged_qc = [&](int k, double* q, double* c) {  // w / theta rows
             const int p = base + k;
@@ -426,9 +451,14 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
             if (row[u] >= 0) {
                 old[u] = __ldg(s.xbar + row[u]);
                 q[u] = __ldg(s.rho + row[u]);
-                xv[u] = __ldg(s.x + row[u]);
                 zv[u] = __ldg(s.z + row[u]);
                 yv[u] = __ldg(s.y + row[u]);
+                if (kZY && (g[u] == 2 || g[u] == 3)) {
+                    xv[u] = gen_row_x(n, row[u], old[u], zv[u], yv[u], q[u]);
+                    s.x[row[u]] = xv[u];
+                } else {
+                    xv[u] = __ldg(s.x + row[u]);
+                }
                 if (kZY) lam[u] = __ldg(s.lambda + row[u]);
             }
         }

@@ -487,7 +487,7 @@ int Session::iterate_ev(double out[4], PhaseTimes* times, cudaEvent_t end_event)
     check(cudaSetDevice(cfg_.device), "cudaSetDevice");
     launch_reset_scalars(sc_, stream_);
     cudaEventRecord(ev_[0], stream_);
-    launch_generators(dn_, ds_, stream_);
+    // the generator projection runs inside the bus kernel (kernels.cu)
     cudaEventRecord(ev_[1], stream_);
     launch_branches(dn_, ds_, branch_cfg(cfg_), sc_, stream_, ev_[5]);
     cudaEventRecord(ev_[2], stream_);
@@ -540,8 +540,7 @@ int Session::iterate_ev(double out[4], PhaseTimes* times, cudaEvent_t end_event)
 void Session::enqueue_x_phase() {
     check(cudaSetDevice(cfg_.device), "cudaSetDevice");
     launch_reset_scalars(sc_, stream_);
-    launch_generators(dn_, ds_, stream_);
-    launch_branches(dn_, ds_, branch_cfg(cfg_), sc_, stream_);
+    launch_branches(dn_, ds_, branch_cfg(cfg_), sc_, stream_);  // generators: in the bus kernel
     check(cudaGetLastError(), "x phase launch");
 }
 

@@ -71,6 +71,15 @@ gridadmm_status gridadmm_network_export(const gridadmm_network* net, double* bus
 gridadmm_status gridadmm_network_partition(const gridadmm_network* net, int k,
                                            int* part_of_bus);
 
+/* Exchange plan of part p of the k-way partition (host only): the rows
+ * whose x part p sends to peer q after the branch phase (and whose xbar, z,
+ * y it gets back after the bus phase), and the rows whose x it receives from
+ * q (and returns).  Branch-major, k = pji, qji, wj, thj per cut branch.  With
+ * NULL row buffers only the counts are written. */
+gridadmm_status gridadmm_network_exchange_rows(const gridadmm_network* net, int k, int p, int q,
+                                               int* send_rows, int* n_send, int* recv_rows,
+                                               int* n_recv);
+
 /* Bus-owned row lists of the coupling layout (proj/src/decomp.cpp:7-31):
  * counts[6*i + k] = sizes of (gen_p, gen_q, flow_p, flow_q, w, theta) of bus
  * i, rows = the lists concatenated per bus in that group order (length m). */

@@ -79,6 +79,7 @@ EXT_SYMBOLS = {
     "gridadmm_network_export": (_I, [_P, _DP, _IP, _DP, _IP, _DP, _IP]),
     "gridadmm_network_layout": (_I, [_P, _IP, _IP]),
     "gridadmm_network_partition": (_I, [_P, _I, _IP]),
+    "gridadmm_network_exchange_rows": (_I, [_P, _I, _I, _I, _IP, _IP, _IP, _IP]),
     "gridadmm_session_new": (_I, [_P, _P, ctypes.POINTER(_P)]),
     "gridadmm_session_free": (None, [_P]),
     "gridadmm_session_solve": (_I, [_P, _P, _I, ctypes.POINTER(_P)]),
@@ -199,6 +200,18 @@ class Network:
         out = np.zeros(max(1, self.num_buses), dtype=np.int32)
         _check(lib().gridadmm_network_partition(self._h, k, out.ctypes.data_as(_IP)))
         return out[: self.num_buses]
+
+    def exchange_rows(self, k: int, p: int, q: int):
+        """(send, recv) row lists of part p toward peer q (gridadmm_network_exchange_rows)."""
+        ns, nr = ctypes.c_int(), ctypes.c_int()
+        _check(lib().gridadmm_network_exchange_rows(self._h, k, p, q, None, ctypes.byref(ns), None,
+                                                    ctypes.byref(nr)))
+        send = np.zeros(max(ns.value, 1), dtype=np.int32)
+        recv = np.zeros(max(nr.value, 1), dtype=np.int32)
+        _check(lib().gridadmm_network_exchange_rows(self._h, k, p, q, send.ctypes.data_as(_IP),
+                                                    ctypes.byref(ns), recv.ctypes.data_as(_IP),
+                                                    ctypes.byref(nr)))
+        return send[:ns.value], recv[:nr.value]
 
     def layout(self):
         counts = np.zeros(6 * self.num_buses, dtype=np.int32)

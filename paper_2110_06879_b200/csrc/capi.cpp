@@ -203,6 +203,21 @@ gridadmm_status gridadmm_network_partition(const gridadmm_network* n, int k, int
     return GRIDADMM_OK;
 }
 
+gridadmm_status gridadmm_network_exchange_rows(const gridadmm_network* n, int k, int p, int q,
+                                               int* send_rows, int* n_send, int* recv_rows,
+                                               int* n_recv) {
+    if (!n || k < 1 || p < 0 || p >= k || q < 0 || q >= k || !n_send || !n_recv)
+        return fail(GRIDADMM_ERR_INVALID_ARG, "bad argument to exchange_rows");
+    return guarded([&]() -> gridadmm_status {
+        const ga::PartPlan pl = ga::make_plan(n->net, ga::partition_buses(n->net, k), p, k);
+        *n_send = static_cast<int>(pl.send_x[q].size());
+        *n_recv = static_cast<int>(pl.recv_x[q].size());
+        if (send_rows) std::memcpy(send_rows, pl.send_x[q].data(), pl.send_x[q].size() * sizeof(int));
+        if (recv_rows) std::memcpy(recv_rows, pl.recv_x[q].data(), pl.recv_x[q].size() * sizeof(int));
+        return GRIDADMM_OK;
+    });
+}
+
 gridadmm_status gridadmm_network_layout(const gridadmm_network* n, int* counts, int* rows) {
     if (!n) return fail(GRIDADMM_ERR_INVALID_ARG, "null network");
     const ga::BusCsr csr = ga::build_bus_csr(n->net);

@@ -25,15 +25,18 @@
 namespace ga {
 
 // Optional path statistics (debug builds with -DGA_TRON_STATS): TRON steps,
-// Cauchy extrapolations, Cauchy halvings, CG iterations, line-search
-// steps, failed Cholesky preconditioners.
+// Cauchy extrapolations, Cauchy halvings evaluated, CG iterations,
+// line-search steps, failed Cholesky preconditioners / fixed points,
+// rejected steps, Cauchy halvings skipped by the pre-screen.
 #ifdef GA_TRON_STATS
 __device__ unsigned long long g_tron_stats[8];  // tron.cuh is included by one TU
 #endif
 #if defined(GA_TRON_STATS) && defined(__CUDA_ARCH__)
 #define GA_STAT(k) atomicAdd(&g_tron_stats[k], 1ull)
+#define GA_STAT_ADD(k, v) atomicAdd(&g_tron_stats[k], (unsigned long long)(v))
 #else
 #define GA_STAT(k) ((void)0)
+#define GA_STAT_ADD(k, v) ((void)0)
 #endif
 
 // Optional section clocks (debug builds with -DGA_STEP_CLOCKS): cycles of
@@ -204,6 +207,84 @@ GA_FN double boundary_tau(const double* s, const double* p, double delta) {
     return tdiv<kOol>(-sp + tsqrt<kOol>(disc), pp);
 }
 
+// ---- exact pre-screen of Cauchy backtracking trials ---------------------
+// The backtracking loop (tron.cpp:127-135) evaluates trials at
+// alpha_k = alpha0 * 2^-k, k = 1..40, and stops at the first k with
+//   ok(s_k) = ||s_k|| <= delta  &&  q(s_k) <= mu0 * g's_k,
+// s_k = clip(x - alpha_k g) - x.  Trials are independent, so a trial whose
+// failure is PROVEN need not be evaluated: the first successful trial, and
+// hence s and every later bit, are unchanged.
+//
+// Proof.  Let P be the components that move (g_i != 0 and not pinned at the
+// bound g pushes against; pinned and g_i == 0 components give s_i = 0
+// exactly).  If no component of P clips at alpha_1 (checked with a margin),
+// none clips at any smaller alpha (x is inside its box and the clamp is
+// monotone), and for every k
+//   s_i = -alpha g_i + e_i,  |e_i| <= d_i = 4u(|x_i| + alpha |g_i|)
+// (rounding of alpha g_i, of x_i - alpha g_i and of the difference;
+// u = 2^-53).  Then with G = sum g_i^2, K = g'Hg over P,
+//   q(s) - mu0 g's = alpha(alpha K / 2 - (1 - mu0) G) + r,
+// where |r| collects the e terms and the rounding of the computed q, g's
+// and of this expression itself; |r| <= err(alpha) below, a polynomial in
+// alpha built from the absolute sums A1 = sum|g_i||x_i|, Hx = sum|g_i||h_ij||x_j|,
+// Kabs = sum|g_i||h_ij||g_j|, Xhx = sum|x_i||h_ij||x_j| with generous
+// constants.  main(alpha) > err(alpha) therefore implies the computed
+// q(s_k) > mu0 g's_k, i.e. trial k fails.  Returns the number of leading
+// trials k = 1, 2, ... so proven (at most 39: the last trial always runs,
+// its step is the result when every trial fails).
+template <int N, class HM>
+GA_FN int cauchy_skip(const double* x, const double* g, const HM& h, const double* l,
+                      const double* u, double alpha0) {
+    constexpr double kU = 1.1102230246251565e-16;  // 2^-53
+    constexpr double kC = (8 * N + 64) * kU;       // first-order rounding constant
+    const double a1 = alpha0 * 0.5;                // largest alpha skipped
+    if (!(alpha0 >= 1e-100)) return 0;             // keep every product a normal number
+    double gm[N], xa[N], ga[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const bool pinned = g[i] == 0.0 || (x[i] <= l[i] && g[i] > 0.0) || (x[i] >= u[i] && g[i] < 0.0);
+        gm[i] = pinned ? 0.0 : g[i];
+        if (!pinned && !(fabs(g[i]) >= 1e-150)) return 0;
+        if (!pinned) {  // x_i - alpha g_i must stay inside [l_i, u_i] for alpha <= a1
+            const double t = x[i] - a1 * g[i];
+            const double m = 8.0 * kU * (fabs(x[i]) + fabs(a1 * g[i]) + fabs(l[i]) + fabs(u[i]));
+            if (!(t - l[i] > m && u[i] - t > m)) return 0;
+        }
+        xa[i] = fabs(x[i]);
+        ga[i] = fabs(gm[i]);
+    }
+    double G = 0.0, K = 0.0, A1 = 0.0, Hx = 0.0, Kabs = 0.0, Xhx = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        G += gm[i] * gm[i];
+        A1 += ga[i] * xa[i];
+        double hg = 0.0, hga = 0.0, hxa = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            const double hij = h[i * N + j], ha = fabs(hij);
+            hg += hij * gm[j];
+            hga += ha * ga[j];
+            hxa += ha * xa[j];
+        }
+        K += gm[i] * hg;
+        Kabs += ga[i] * hga;
+        Hx += ga[i] * hxa + xa[i] * hga;  // both orders: the computed H need not be symmetric
+        Xhx += xa[i] * hxa;
+    }
+    if (!(K > 0.0) || !(Kabs >= 1e-250) || !sfinite(Kabs) || !sfinite(Xhx)) return 0;
+    const double c1 = 1.0 - kTronMu0;
+    double a = alpha0;
+    int k = 0;
+    for (; k < 39; ++k) {
+        a *= 0.5;  // alpha_{k+1}
+        const double main = a * (0.5 * a * K - c1 * G);
+        const double err = kC * (A1 + a * (G + Hx) + a * a * Kabs) +
+                           64.0 * kU * kU * (Xhx + 2.0 * a * Hx + a * a * Kabs);
+        if (!(main > 1.0625 * err)) break;
+    }
+    return k;
+}
+
 // Cauchy point (tron.cpp:101-137).
 template <int N, bool kOol, class HM>
 GA_FN void cauchy_point(const double* x, const double* g, const HM& h,
@@ -258,6 +339,12 @@ GA_FN void cauchy_point(const double* x, const double* g, const HM& h,
             a = a * 2.0;
         } else {
             if (cnt >= 40) return;
+            if (cnt == 0) {  // trial 0 failed: jump over the proven failures
+                const int sk = cauchy_skip<N>(x, g, h, l, u, a);
+                GA_STAT_ADD(7, sk);
+                for (int j = 0; j < sk; ++j) a *= 0.5;
+                cnt += sk;
+            }
             GA_STAT(2);
             a *= 0.5;
         }
@@ -483,19 +570,22 @@ struct TileSearch {
             return;
         }
         const double alpha0 = smin(1.0, delta / gnorm);
+        // backtracking trials k = 1..sk are proven failures (cauchy_skip):
+        // the backtracking lanes start at k = sk + 1
+        const int sk = cauchy_skip<N>(x, g, h, l, u, alpha0);
         double mys[N];
         // One trial site and one broadcast site (code size: this runs in a
         // persistent kernel whose hot loop must stay in the instruction cache).
         // Candidate exponents c (trial at alpha0 * 2^c):
-        //   round 0: rank 0 -> 0, rank 1 -> +1, ranks 2.. -> -1, -2, ...
+        //   round 0: rank 0 -> 0, rank 1 -> +1, ranks 2.. -> -(sk+1), -(sk+2), ...
         //   extrapolation rounds r >= 1: 2 + (r-1)*T + rank   (valid <= 20)
-        //   backtracking rounds r >= 1: -((T-1) + (r-1)*T + rank) (valid >= -40)
+        //   backtracking rounds r >= 1: -(sk + (T-1) + (r-1)*T + rank) (valid >= -40)
         int dir = 0;  // +1 extrapolating, -1 backtracking (decided in round 0)
         for (int round = 0;; ++round) {
             int c;
-            if (round == 0) c = rank == 0 ? 0 : (rank == 1 ? 1 : -(rank - 1));
+            if (round == 0) c = rank == 0 ? 0 : (rank == 1 ? 1 : -(sk + rank - 1));
             else if (dir > 0) c = 2 + (round - 1) * T + rank;
-            else c = -((T - 1) + (round - 1) * T + rank);
+            else c = -(sk + (T - 1) + (round - 1) * T + rank);
             const bool valid = dir > 0 ? c <= 20 : c >= -40;
             bool okc = false, mok = false;
             double mv = 0.0;
@@ -523,6 +613,7 @@ struct TileSearch {
                     dir = -1;
                     const unsigned hm = okm >> 2;
                     if (hm) src = __ffs(hm) - 1 + 2;
+                    else if (sk + T - 2 >= 40) src = 41 - sk;  // k = 40 was tried: its step
                     else done = false;
                 }
             } else if (dir > 0) {
@@ -530,7 +621,7 @@ struct TileSearch {
                 if (run > 0) src = run - 1;
                 done = run < T;  // a failure (or the c > 20 limit) ended the run
             } else {
-                const int kb = (T - 1) + (round - 1) * T;  // this round tried k = kb..kb+T-1
+                const int kb = sk + (T - 1) + (round - 1) * T;  // this round tried k = kb..kb+T-1
                 if (okm) src = __ffs(okm) - 1;
                 else if (kb + T - 1 >= 40) src = 40 - kb;  // none up to 2^-40: last trial's step
                 else done = false;
@@ -630,7 +721,6 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
     } else {
         GA_STAT(6);  // rejected step: x (hence g, H) unchanged
     }
-    if (st.iter >= 100) GA_STAT(7);  // steps of solves deep in the tail
     ++st.iter;
     // Fixed point: a rejected step that leaves the radius bit-identical
     // leaves the whole iterate (x, f, delta) unchanged, and an iteration with

@@ -314,8 +314,13 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
 #ifndef GA_TILE_MINB
 #define GA_TILE_MINB 1
 #endif
+__device__ __forceinline__ bool gate_closed(const BranchCfg& cfg) {
+    return cfg.gate && *reinterpret_cast<const volatile int*>(&cfg.gate->stop);
+}
+
 __global__ void __launch_bounds__(kLaneBlock, GA_LANE_MINB) lane_kernel(DevNet net, DevState st, BranchCfg cfg,
                                                           Work w, DevScalars* sc) {
+    if (gate_closed(cfg)) return;
     extern __shared__ double smem[];
     unsigned long long it6 = 0, it4 = 0;
     int fails = 0;
@@ -442,6 +447,7 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
 
 __global__ void __launch_bounds__(kTileBlock, GA_TILE_MINB) tile_kernel(DevNet net, DevState st, BranchCfg cfg,
                                                           Work w, DevScalars* sc) {
+    if (gate_closed(cfg)) return;
     __shared__ double smem[kFields * (kTileBlock / kTile)];
     unsigned long long it6 = 0, it4 = 0;
     int fails = 0;
@@ -493,6 +499,7 @@ __global__ void __launch_bounds__(kTileBlock, GA_TILE_MINB) tile_kernel(DevNet n
 // diverging in the warp) in a block of its own.
 __global__ void __launch_bounds__(kSoloBlock) solo_kernel(DevNet net, DevState st, BranchCfg cfg,
                                                           Work w, DevScalars* sc) {
+    if (gate_closed(cfg)) return;
     __shared__ double smem[kFields * (kTileBlock / kTile)];
     unsigned long long it6 = 0, it4 = 0;
     int fails = 0;
@@ -674,26 +681,39 @@ const int* branch_overflow_counts(const DevNet& n, const DevState& s) {
     return work_of(n, s).ctr + 2;
 }
 
-void launch_branches(const DevNet& n, const DevState& s, const BranchCfg& cfg, DevScalars* sc,
-                     cudaStream_t st, cudaEvent_t mid) {
-    if (n.nl <= 0) return;
-    const Work w = work_of(n, s);
-    cudaMemsetAsync(w.ctr, 0, kCounters * sizeof(int), st);
-    const size_t lane_smem =
-        static_cast<size_t>(kFields) * kLaneBlock * sizeof(double);
-    // persistent grid sizes (thread-safe one-time init; the pool's GPUs are identical)
-    struct Grids {
-        int lane, tile, solo;
-    };
-    static const Grids grids = [lane_smem] {
+namespace {
+
+constexpr size_t kLaneSmem = static_cast<size_t>(kFields) * kLaneBlock * sizeof(double);
+
+struct Grids {
+    int lane, tile, solo;
+};
+
+// persistent grid sizes (thread-safe one-time init; the pool's GPUs are identical)
+const Grids& branch_grids() {
+    static const Grids grids = [] {
         Grids gr;
-        gr.lane = persistent_blocks(lane_kernel, kLaneBlock, lane_smem);
+        gr.lane = persistent_blocks(lane_kernel, kLaneBlock, kLaneSmem);
         gr.tile = persistent_blocks(tile_kernel, kTileBlock, 0);
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&gr.solo, cudaDevAttrMultiProcessorCount, dev);
         return gr;
     }();
+    return grids;
+}
+
+}  // namespace
+
+void prepare_branch_launch() { (void)branch_grids(); }
+
+void launch_branches(const DevNet& n, const DevState& s, const BranchCfg& cfg, DevScalars* sc,
+                     cudaStream_t st, cudaEvent_t mid) {
+    if (n.nl <= 0) return;
+    const Work w = work_of(n, s);
+    cudaMemsetAsync(w.ctr, 0, kCounters * sizeof(int), st);
+    const size_t lane_smem = kLaneSmem;
+    const Grids& grids = branch_grids();
     const int lane_blocks = grids.lane, tile_blocks = grids.tile, solo_blocks = grids.solo;
     const int total = n.n_lim + n.n_unl;
     const int need = (total + kLaneBlock - 1) / kLaneBlock;

@@ -109,6 +109,31 @@ struct DevExtract {
     ExtractScalars* sc = nullptr;
 };
 
+// Device-side inner-loop control (solve.cpp's graph path): the stop tests of
+// driver.cpp:186-220 evaluated on the device after every iteration, so a
+// CUDA graph of several iterations runs without a host round trip; kernels
+// of iterations after a stop see `stop` and return at entry.
+enum LoopStop : int { kLoopRunning = 0, kLoopInner = 1, kLoopLimit = 2, kLoopDiverged = 3,
+                      kLoopSingular = 4 };
+struct LoopCtl {
+    // inputs, written by the host before each outer iteration
+    double inner_tol, eps, diverge, rho_max, beta;
+    int outer, max_inner;
+    // state
+    int inner;      // inner iterations done in this outer iteration
+    int stop;       // LoopStop
+    int singular;   // internal index of the singular bus (kLoopSingular)
+    int pad;
+    unsigned long long failures;  // branch failures in this outer iteration
+    double last_z;                // ||z||_inf of the last iteration
+    unsigned long long t_start, t_mark, t_bus, x_ns, xbar_ns;  // %globaltimer stamps / phase sums
+};
+struct LoopRec {  // one IterationRecord (driver.cpp:190) with a device timestamp
+    int outer, inner;
+    double primal, dual, z, drift;
+    unsigned long long t_ns;
+};
+
 struct BranchCfg {
     double gtol = 1e-6;
     int max_iterations = 200;
@@ -121,6 +146,7 @@ struct BranchCfg {
     int tile_slots = 0;   // set by the launcher: tiles available per queue
     int tail_num = 2;     // whole-warp tiles when a queue <= tail_num/4 of the grid's warps
     int tile_budget = 48; // steps in the 8-lane tile phase before the solo phase takes over (0 = off)
+    const LoopCtl* gate = nullptr;  // graph path: skip the launch when gate->stop
 };
 
 // ---- launchers (kernels.cu / branch.cu) ----------------------------------
@@ -130,12 +156,21 @@ void launch_generators(const DevNet& n, const DevState& s, cudaStream_t st);
 // `mid` (optional) is recorded between the lane-phase and tile-phase kernels.
 void launch_branches(const DevNet& n, const DevState& s, const BranchCfg& cfg,
                      DevScalars* sc, cudaStream_t st, cudaEvent_t mid = nullptr);
+// One-time launch setup of the branch kernels (grid sizes, smem attribute);
+// called before a stream capture, where such calls are not allowed.
+void prepare_branch_launch();
 // Overflow queue sizes (6-var, 4-var) of the last branch sweep (device ints).
 const int* branch_overflow_counts(const DevNet& n, const DevState& s);
 void launch_buses(const DevNet& n, const DevState& s, DevScalars* sc, cudaStream_t st);
-// Bus QP fused with z, y and all four residual norms (the iteration path).
+// Bus QP fused with the generator projection, z, y and all four residual
+// norms (the iteration path).  With a gate (graph path) beta is read from
+// gate->beta and the launch is a no-op once gate->stop is set.
 void launch_bus_zy(const DevNet& n, const DevState& s, double beta, DevScalars* sc,
-                   cudaStream_t st);
+                   cudaStream_t st, LoopCtl* gate = nullptr);
+// Graph path: stamp the loop start and clear the scalars / the control
+// kernel after each iteration (records, stop tests, scalar reset).
+void launch_loop_start(LoopCtl* ctl, DevScalars* sc, cudaStream_t st);
+void launch_loop_control(LoopCtl* ctl, LoopRec* rec, DevScalars* sc, cudaStream_t st);
 // Separate z / y phases (phase-replay API).
 void launch_z_only(const DevNet& n, const DevState& s, double beta, cudaStream_t st);
 void launch_y_only(const DevNet& n, const DevState& s, cudaStream_t st);

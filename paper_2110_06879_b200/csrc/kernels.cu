@@ -202,9 +202,20 @@ __device__ __forceinline__ int group_of(const int* gl, int k) {
 
 constexpr int kFlagNonfinite = 1, kFlagSingular = 2, kFlagRef = 4;
 
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 template <bool kZY>
 __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, double beta,
-                                                       DevScalars* sc) {
+                                                       DevScalars* sc, LoopCtl* gate) {
+    if (gate) {
+        if (*reinterpret_cast<volatile int*>(&gate->stop)) return;
+        beta = gate->beta;
+        if (blockIdx.x == 0 && threadIdx.x == 0) gate->t_bus = global_ns();
+    }
     __shared__ int s_off[kBB + 1];
     __shared__ int s_base[kBB];
     __shared__ int s_gl[kBB][8];  // local group offsets 0..6, [7] = flags
@@ -556,6 +567,70 @@ __global__ void reset_scalars_kernel(DevScalars* sc) {
 
 inline int blocks_for(int n) { return (n + kBlock - 1) / kBlock; }
 
+__device__ __forceinline__ double from_bits_dev(unsigned long long b) {
+    return __longlong_as_double(static_cast<long long>(b));
+}
+
+__global__ void loop_start_kernel(LoopCtl* c, DevScalars* sc) {
+    c->t_start = global_ns();
+    c->t_mark = c->t_start;
+    c->t_bus = c->t_start;
+    sc->primal_inf = 0;
+    sc->dual_inf = 0;
+    sc->z_inf = 0;
+    sc->z_drift = 0;
+    sc->failures = 0;
+    sc->singular_bus = INT_MAX;
+}
+
+// driver.cpp:179-220 after one iteration: the record, then the divergence
+// and inner stop tests in the reference's order; clears the scalars for the
+// next iteration.  One thread.
+__global__ void loop_control_kernel(LoopCtl* c, LoopRec* rec, DevScalars* sc) {
+    if (c->stop) return;
+    const unsigned long long now = global_ns();
+    if (sc->singular_bus != INT_MAX) {
+        c->singular = sc->singular_bus;
+        c->stop = kLoopSingular;
+        return;
+    }
+    const double primal = from_bits_dev(sc->primal_inf);
+    const double dual = from_bits_dev(sc->dual_inf) * c->rho_max;
+    const double z = from_bits_dev(sc->z_inf);
+    const double drift = from_bits_dev(sc->z_drift);
+    const int inner = ++c->inner;
+    LoopRec r;
+    r.outer = c->outer;
+    r.inner = inner;
+    r.primal = primal;
+    r.dual = dual;
+    r.z = z;
+    r.drift = drift;
+    r.t_ns = now;
+    rec[inner - 1] = r;
+    c->failures += sc->failures;
+    c->x_ns += c->t_bus - c->t_mark;
+    c->xbar_ns += now - c->t_bus;
+    c->t_mark = now;
+    c->last_z = z;
+    int stop = kLoopRunning;
+    if (!sfinite(primal) || !sfinite(dual) || primal > c->diverge || dual > c->diverge)
+        stop = kLoopDiverged;
+    else if (smax(primal, dual) <= c->inner_tol)
+        stop = kLoopInner;
+    else if (primal <= c->inner_tol && z <= c->eps && drift <= 0.01 * c->eps)
+        stop = kLoopInner;
+    else if (inner >= c->max_inner)
+        stop = kLoopLimit;
+    c->stop = stop;
+    sc->primal_inf = 0;
+    sc->dual_inf = 0;
+    sc->z_inf = 0;
+    sc->z_drift = 0;
+    sc->failures = 0;
+    sc->singular_bus = INT_MAX;
+}
+
 // FP64 pipe microbenchmark: 8 independent chains per thread.  kFma = false
 // issues DMUL + DADD (what -fmad=false code runs), true issues DFMA.
 template <bool kFma>
@@ -620,13 +695,13 @@ void launch_generators(const DevNet& n, const DevState& s, cudaStream_t st) {
 
 void launch_buses(const DevNet& n, const DevState& s, DevScalars* sc, cudaStream_t st) {
     const int c = n.buses_count();
-    if (c > 0) bus_block_kernel<false><<<(c + kBB - 1) / kBB, kBB, 0, st>>>(n, s, 0.0, sc);
+    if (c > 0) bus_block_kernel<false><<<(c + kBB - 1) / kBB, kBB, 0, st>>>(n, s, 0.0, sc, nullptr);
 }
 
 void launch_bus_zy(const DevNet& n, const DevState& s, double beta, DevScalars* sc,
-                   cudaStream_t st) {
+                   cudaStream_t st, LoopCtl* gate) {
     const int c = n.buses_count();
-    if (c > 0) bus_block_kernel<true><<<(c + kBB - 1) / kBB, kBB, 0, st>>>(n, s, beta, sc);
+    if (c > 0) bus_block_kernel<true><<<(c + kBB - 1) / kBB, kBB, 0, st>>>(n, s, beta, sc, gate);
 }
 
 void launch_z_only(const DevNet& n, const DevState& s, double beta, cudaStream_t st) {
@@ -684,6 +759,14 @@ void launch_scatter_rows(const int* rows, int count, const double* buf, double* 
 void launch_rowmax(const double* v, int n, unsigned long long* dst, cudaStream_t st) {
     cudaMemsetAsync(dst, 0, sizeof(unsigned long long), st);
     if (n > 0) rowmax_kernel<<<64, kBlock, 0, st>>>(v, n, dst);
+}
+
+void launch_loop_start(LoopCtl* ctl, DevScalars* sc, cudaStream_t st) {
+    loop_start_kernel<<<1, 1, 0, st>>>(ctl, sc);
+}
+
+void launch_loop_control(LoopCtl* ctl, LoopRec* rec, DevScalars* sc, cudaStream_t st) {
+    loop_control_kernel<<<1, 1, 0, st>>>(ctl, rec, sc);
 }
 
 void launch_reset_scalars(DevScalars* sc, cudaStream_t st) {

@@ -102,6 +102,15 @@ void Session::free_all() {
     if (!allocs_.empty() && stream_) cudaStreamSynchronize(stream_);
     allocs_.clear();
     if (sc_host_) pinned_slot_release(sc_host_);
+    if (ctl_host_) pinned_slot_release(ctl_host_);
+    ctl_host_ = nullptr;
+    if (rec_host_) cudaFreeHost(rec_host_);
+    rec_host_ = nullptr;
+    if (graph_) cudaGraphExecDestroy(graph_);
+    graph_ = nullptr;
+    ctl_ = nullptr;
+    rec_ = nullptr;
+    rec_cap_ = 0;
     if (flush_buf_) cudaFree(flush_buf_);
     flush_buf_ = nullptr;
     sc_ = nullptr;
@@ -328,6 +337,93 @@ void Session::download_solution_inputs(std::vector<double>& gen_rows, std::vecto
                               cudaMemcpyDeviceToHost, stream_), "D2H");
     }
     check(cudaStreamSynchronize(stream_), "sync");
+}
+
+BranchCfg branch_cfg(const SolverConfig& c);
+
+// The graph path of Algorithm 1's inner loop (driver.cpp:155-220).  One
+// captured batch = kGraphIters iterations, each: branch kernels, the fused
+// bus kernel, the control kernel; every kernel is gated on ctl->stop, so the
+// iterations after a stop are empty launches and the state is exactly that
+// of the stopping iteration.  The host reads the control block and the new
+// records once per batch instead of the norms once per iteration.
+bool Session::inner_loop(const SolverConfig& cfg, int outer, double rho_max, double inner_tol,
+                         double elapsed_s, SolveReport& rep, int* stop, double* last_z) {
+    if (plan_.parts > 1 || prof_ || dn_.nl <= 0) return false;
+    use_device();
+    if (!ctl_) {
+        check(cudaMallocAsync(reinterpret_cast<void**>(&ctl_), sizeof(LoopCtl), stream_), "ctl alloc");
+        allocs_.push_back(ctl_);
+        ctl_host_ = static_cast<LoopCtl*>(pinned_slot_acquire());
+        check(cudaMallocHost(reinterpret_cast<void**>(&rec_host_), kGraphIters * sizeof(LoopRec)),
+              "cudaMallocHost records");
+    }
+    if (rec_cap_ < cfg.max_inner) {
+        check(cudaMallocAsync(reinterpret_cast<void**>(&rec_), cfg.max_inner * sizeof(LoopRec), stream_),
+              "records alloc");
+        allocs_.push_back(rec_);
+        rec_cap_ = cfg.max_inner;
+        if (graph_) cudaGraphExecDestroy(graph_);  // the control kernels hold the old pointer
+        graph_ = nullptr;
+    }
+    if (!graph_) {
+        BranchCfg bc = branch_cfg(cfg_);
+        bc.gate = ctl_;
+        cudaGraph_t g = nullptr;
+        prepare_branch_launch();
+        check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture begin");
+        for (int k = 0; k < kGraphIters; ++k) {
+            launch_branches(dn_, ds_, bc, sc_, stream_);
+            launch_bus_zy(dn_, ds_, beta_, sc_, stream_, ctl_);
+            launch_loop_control(ctl_, rec_, sc_, stream_);
+        }
+        check(cudaStreamEndCapture(stream_, &g), "capture end");
+        check(cudaGraphInstantiate(&graph_, g, 0), "graph instantiate");
+        cudaGraphDestroy(g);
+    }
+    LoopCtl& h = *ctl_host_;
+    std::memset(&h, 0, sizeof h);
+    h.inner_tol = inner_tol;
+    h.eps = cfg.eps;
+    h.diverge = cfg.divergence_threshold;
+    h.rho_max = rho_max;
+    h.beta = beta_;
+    h.outer = outer;
+    h.max_inner = cfg.max_inner;
+    check(cudaMemcpyAsync(ctl_, &h, sizeof h, cudaMemcpyHostToDevice, stream_), "ctl upload");
+    launch_loop_start(ctl_, sc_, stream_);
+    check(cudaGetLastError(), "loop start");
+    int done = 0;
+    unsigned long long t_start = 0;
+    for (;;) {
+        check(cudaGraphLaunch(graph_, stream_), "graph launch");
+        const int window = std::min(kGraphIters, cfg.max_inner - done);
+        check(cudaMemcpyAsync(ctl_host_, ctl_, sizeof(LoopCtl), cudaMemcpyDeviceToHost, stream_), "D2H");
+        if (window > 0)
+            check(cudaMemcpyAsync(rec_host_, rec_ + done, window * sizeof(LoopRec),
+                                  cudaMemcpyDeviceToHost, stream_), "D2H");
+        check(cudaStreamSynchronize(stream_), "graph sync");
+        if (!t_start) t_start = h.t_start;
+        const int n = h.inner;
+        for (int i = done; i < n; ++i) {
+            const LoopRec& r = rec_host_[i - done];
+            rep.series.push_back({r.outer, r.inner, r.primal, r.dual, r.z,
+                                  elapsed_s + 1e-9 * static_cast<double>(r.t_ns - t_start)});
+        }
+        done = n;
+        if (h.stop != kLoopRunning) break;
+    }
+    if (h.stop == kLoopSingular) {
+        const int id = net_.buses[h.singular].id;
+        throw SingularBusError(id, "isolated bus " + std::to_string(id) + ": singular balance system");
+    }
+    rep.inner_iterations += done;
+    rep.branch_solve_failures += static_cast<int>(h.failures);
+    rep.phase_times.x_s += 1e-9 * static_cast<double>(h.x_ns);
+    rep.phase_times.xbar_s += 1e-9 * static_cast<double>(h.xbar_ns);
+    *stop = h.stop;
+    *last_z = h.last_z;
+    return true;
 }
 
 bool Session::extract_on_device(Solution& sol, QualityMetrics& q) {

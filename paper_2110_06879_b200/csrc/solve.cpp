@@ -183,25 +183,38 @@ SolveReport solve(Engine& s, const SolverConfig& cfg, bool warm) {
 
     for (int outer = 1; outer <= cfg.max_outer; ++outer) {
         report.outer_iterations = outer;
-        for (int inner = 1; inner <= cfg.max_inner; ++inner) {
-            double nrm[4];
-            report.branch_solve_failures += s.iterate(nrm, &report.phase_times);
-            const double primal = nrm[0];
-            const double dual = nrm[1] * rho_max;
-            const double z_inf = nrm[2];
-            last_z_inf = z_inf;
-            ++report.inner_iterations;
-            report.series.push_back({outer, inner, primal, dual, z_inf, seconds_since(t0)});
-            if (!sfinite(primal) || !sfinite(dual) || primal > cfg.divergence_threshold ||
-                dual > cfg.divergence_threshold) {
+        int stop = 0;
+        if (s.inner_loop(cfg, outer, rho_max, inner_tol, seconds_since(t0), report, &stop,
+                         &last_z_inf)) {
+            if (stop == kLoopDiverged) {
+                const IterationRecord& r = report.series.back();
                 report.status = SolveStatus::Diverged;
                 report.diagnostic = "residual norm exceeded divergence threshold at outer " +
-                                    std::to_string(outer) + " inner " + std::to_string(inner);
+                                    std::to_string(r.outer) + " inner " + std::to_string(r.inner);
                 finish_report(s, report);
                 return report;
             }
-            if (smax(primal, dual) <= inner_tol) break;
-            if (primal <= inner_tol && z_inf <= cfg.eps && nrm[3] <= 0.01 * cfg.eps) break;
+        } else {
+            for (int inner = 1; inner <= cfg.max_inner; ++inner) {
+                double nrm[4];
+                report.branch_solve_failures += s.iterate(nrm, &report.phase_times);
+                const double primal = nrm[0];
+                const double dual = nrm[1] * rho_max;
+                const double z_inf = nrm[2];
+                last_z_inf = z_inf;
+                ++report.inner_iterations;
+                report.series.push_back({outer, inner, primal, dual, z_inf, seconds_since(t0)});
+                if (!sfinite(primal) || !sfinite(dual) || primal > cfg.divergence_threshold ||
+                    dual > cfg.divergence_threshold) {
+                    report.status = SolveStatus::Diverged;
+                    report.diagnostic = "residual norm exceeded divergence threshold at outer " +
+                                        std::to_string(outer) + " inner " + std::to_string(inner);
+                    finish_report(s, report);
+                    return report;
+                }
+                if (smax(primal, dual) <= inner_tol) break;
+                if (primal <= inner_tol && z_inf <= cfg.eps && nrm[3] <= 0.01 * cfg.eps) break;
+            }
         }
         // ||z||_inf of the state after the inner loop == the last record's
         const double z_inf = last_z_inf;

@@ -137,6 +137,15 @@ public:
     // Solution extraction + quality metrics on the device (extract.cu);
     // false when this engine leaves them to the host (multi-part engines).
     virtual bool extract_on_device(Solution& sol, QualityMetrics& q) { return false; }
+    // The inner loop of one outer iteration as CUDA graphs of several
+    // iterations with the stop tests on the device (no host round trip per
+    // iteration).  Appends the records, counts and phase times to `rep`;
+    // *stop = LoopStop, *last_z = ||z||_inf of the last iteration.  Returns
+    // false when this engine runs the host loop instead.
+    virtual bool inner_loop(const SolverConfig& cfg, int outer, double rho_max, double inner_tol,
+                            double elapsed_s, SolveReport& rep, int* stop, double* last_z) {
+        return false;
+    }
     virtual int parts() const { return 1; }
     // k iterations each bracketed by CUDA events (see Session::timed_steps)
     virtual int timed_steps(int k, size_t flush_bytes, double* step_ms, double* records) = 0;
@@ -208,6 +217,8 @@ public:
     void sync() const;
 
     bool extract_on_device(Solution& sol, QualityMetrics& q) override;
+    bool inner_loop(const SolverConfig& cfg, int outer, double rho_max, double inner_tol,
+                    double elapsed_s, SolveReport& rep, int* stop, double* last_z) override;
     // Solution extraction inputs: x gen rows, bus_w, bus_theta.
     void download_solution_inputs(std::vector<double>& gen_rows, std::vector<double>& w,
                                   std::vector<double>& th) const override;
@@ -221,6 +232,14 @@ private:
     DevNet dn_;
     DevState ds_;
     DevExtract ext_;  // single-part sessions only
+    // graph path (inner_loop): control block, records, the captured batch
+    LoopCtl* ctl_ = nullptr;
+    LoopCtl* ctl_host_ = nullptr;  // pinned
+    LoopRec* rec_ = nullptr;
+    LoopRec* rec_host_ = nullptr;  // pinned
+    int rec_cap_ = 0;
+    cudaGraphExec_t graph_ = nullptr;
+    static constexpr int kGraphIters = 16;
     DevScalars* sc_ = nullptr;       // device
     DevScalars* sc_host_ = nullptr;  // pinned mirror
     unsigned long long* red_ = nullptr;

@@ -27,6 +27,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REF_SO = os.path.join(HERE, "_ref", "libgridadmm_ref.so")
+# the same reference objects linked against glibc's own sincos (no pin)
+STOCK_SO = os.path.join(HERE, "_ref", "libgridadmm_stock.so")
 PORT_SO = os.path.join(HERE, "liboracle.so")
 REF_SRC = "/root/reference/proj/src"
 
@@ -229,6 +231,45 @@ def ref_capi():
         fn.restype = res
         fn.argtypes = args
     return h
+
+
+_STOCK = None
+
+
+def have_stock() -> bool:
+    return os.path.exists(STOCK_SO)
+
+
+def stock_capi():
+    """The reference's C ABI from _ref/libgridadmm_stock.so: the unmodified
+    reference with glibc's sincos (host-dependent bits; compared with the
+    pinned build and the product at tolerance only)."""
+    global _STOCK
+    if _STOCK is None:
+        h = ctypes.CDLL(STOCK_SO)
+        for name, (res, args) in REF_SYMBOLS.items():
+            fn = getattr(h, name)
+            fn.restype = res
+            fn.argtypes = args
+        _STOCK = h
+    return _STOCK
+
+
+def capi_solve(h, case_path: str, **cfg):
+    """gridadmm_solve through a reference C ABI handle; returns (status, metrics)."""
+    net = ctypes.c_void_p()
+    assert h.gridadmm_network_load(os.fsencode(case_path), ctypes.byref(net)) == 0
+    c = h.gridadmm_config_new()
+    for k, v in cfg.items():
+        assert h.gridadmm_config_set(c, k.encode(), float(v)) == 0, k
+    rep = ctypes.c_void_p()
+    st = h.gridadmm_solve(net, c, ctypes.byref(rep))
+    m = ref_metrics(h, rep) if rep.value else {}
+    if rep.value:
+        h.gridadmm_report_free(rep)
+    h.gridadmm_config_free(c)
+    h.gridadmm_network_free(net)
+    return st, m
 
 
 def ref_metrics(h, rep) -> Dict[str, float]:

@@ -490,6 +490,7 @@ GA_FN bool tron_begin(const P& prob, TronState<N>& st) {
     st.f = prob.value(st.x);
     st.delta = 0.0;
     st.iter = 0;
+    if constexpr (P::kGhCache) prob.gh_set(false);
     return sfinite(st.f);
 }
 
@@ -673,17 +674,31 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
     for (int i = 0; i < N; ++i) { l[i] = prob.lo(i); u[i] = prob.hi(i); }
     GA_CLK_DECL
     double g[N];
-    prob.gradient(st.x, g);
-#pragma unroll
-    for (int i = 0; i < N; ++i)
-        if (!sfinite(g[i])) return kStepError;
-    if (proj_grad_norm<N>(st.x, g, l, u) <= cfg.gtol) return kStepConverged;
-    GA_CLK(0);
     double h[N * N];
-    search.template hessian<N>(prob, st.x, h);
+    if (prob.gh_cached()) {  // rejected last step: x, hence g and H, unchanged
 #pragma unroll
-    for (int i = 0; i < N * N; ++i)
-        if (!sfinite(h[i])) return kStepError;
+        for (int i = 0; i < N; ++i) g[i] = prob.cache_g(i);
+        if (proj_grad_norm<N>(st.x, g, l, u) <= cfg.gtol) return kStepConverged;
+#pragma unroll
+        for (int i = 0; i < N * N; ++i) h[i] = prob.cache_h(i);
+    } else {
+        prob.gradient(st.x, g);
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+            if (!sfinite(g[i])) return kStepError;
+        if (proj_grad_norm<N>(st.x, g, l, u) <= cfg.gtol) return kStepConverged;
+        GA_CLK(0);
+        search.template hessian<N>(prob, st.x, h);
+#pragma unroll
+        for (int i = 0; i < N * N; ++i)
+            if (!sfinite(h[i])) return kStepError;
+        if constexpr (P::kGhCache) {
+#pragma unroll
+            for (int i = 0; i < N; ++i) prob.cache_put_g(i, g[i]);
+#pragma unroll
+            for (int i = 0; i < N * N; ++i) prob.cache_put_h(i, h[i]);
+        }
+    }
     constexpr bool kOol = Search::kOolDivSqrt;
     if (st.iter == 0 && st.delta == 0.0) st.delta = smax(vnorm2<N, kOol>(g), cfg.delta_floor);
 
@@ -714,6 +729,7 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
     if (ratio < 0.25) st.delta = 0.25 * smax(snorm, 1e-12);
     else if (ratio > 0.75 && snorm >= 0.9 * st.delta) st.delta = smin(2.0 * st.delta, kTronDeltaMax);
     const bool accepted = ared > 0.0 && ratio > kTronEta;
+    if constexpr (P::kGhCache) prob.gh_set(!accepted);
     if (accepted) {
 #pragma unroll
         for (int i = 0; i < N; ++i) st.x[i] = xt[i];

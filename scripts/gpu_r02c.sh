@@ -5,7 +5,7 @@ mkdir -p gpurun_out/c
 O=gpurun_out/c
 timeout 2400 python -m pytest tests -m gpu -q --timeout=900 > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
-for v in stage8 stage12; do GRIDADMM_LIB=paper_2110_06879_b200/libgridadmm_$v.so timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-converge --no-track > $O/bench_$v.json 2>&1; done
+for v in stage8 stage12 ghc; do GRIDADMM_LIB=paper_2110_06879_b200/libgridadmm_$v.so timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-converge --no-track > $O/bench_$v.json 2>&1; done
 timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-converge --no-track > $O/bench_stage16.json 2>&1
 GRIDADMM_LIB=paper_2110_06879_b200/libgridadmm_stats.so timeout 600 python scripts/probe_path_stats.py case_ACTIVSg70k case_ACTIVSg70k 5 20 > $O/stats_70k_5.json 2>&1
 GRIDADMM_LIB=paper_2110_06879_b200/libgridadmm_stats.so timeout 600 python scripts/probe_path_stats.py case_ACTIVSg70k case_ACTIVSg70k 3000 20 > $O/stats_70k_3000.json 2>&1

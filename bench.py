@@ -384,9 +384,17 @@ def run_track(ga, dev):
            "c_inf_max": float(max(p["c_inf"] for p in per)) if per else None}
     ref = _load_json(TRACK_CPU_FILE)
     if ref:
-        out["cpu_warm_s_per_step_mean"] = ref.get("cpu_warm_s_per_step_mean")
+        k = int(ref.get("cpu_periods") or 0)
+        cpu_mean = ref.get("cpu_warm_s_per_step_mean")
+        out["cpu_warm_s_per_step_mean"] = cpu_mean
+        out["cpu_periods"] = k
         out["cpu_cores"] = ref.get("cpu_cores")
         out["cpu_source"] = os.path.relpath(TRACK_CPU_FILE, REPO)
+        out["cpu_objectives_bit_identical"] = ref.get("objectives_bit_identical")
+        if k > 1 and cpu_mean and len(warm) >= k - 1:
+            gm = float(np.mean(warm[:k - 1]))  # the same warm snapshots the CPU ran
+            out["gpu_warm_s_per_step_mean_same_periods"] = gm
+            out["warm_speedup_vs_cpu_same_periods"] = cpu_mean / gm
     return out
 
 

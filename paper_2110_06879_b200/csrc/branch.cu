@@ -71,11 +71,6 @@ constexpr double kAlShrink = 0.25;
 constexpr double kRhoTildeMax = 1e7;
 
 constexpr int kLaneBlock = 128;  // lane phase: one slot per thread
-#ifndef GA_LANE_GH_CACHE
-#define GA_LANE_GH_CACHE 0
-#endif
-constexpr bool kLaneCache = GA_LANE_GH_CACHE != 0;  // gradient / Hessian cache in the lane slot
-constexpr int kLaneFields = kLaneCache ? kFieldsCache : kFields;
 constexpr int kTileBlock = 128;  // tile phase: one slot per tile
 #ifndef GA_TILE
 #define GA_TILE 8
@@ -213,7 +208,7 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
     const int lane = threadIdx.x & 31;
     unsigned my_exec = 0;  // trust-region steps executed by this lane
     const Slot<kLaneBlock> slot{smem + threadIdx.x};
-    BranchProb<N, kLaneBlock, kLaneCache> p{slot};
+    BranchProb<N, kLaneBlock> p{slot};
     const TronParams tp = tron_params(cfg);
     const double kInf = __longlong_as_double(0x7ff0000000000000LL);
 
@@ -522,13 +517,6 @@ __global__ void __launch_bounds__(kSoloBlock) solo_kernel(DevNet net, DevState s
 // Dense box QP for the TRON-core parity test (proj/tests/acceptance.cpp:458-520).
 template <int N>
 struct QpProb {
-    static constexpr bool kGhCache = false;
-    GA_FN bool gh_cached() const { return false; }
-    GA_FN void gh_set(bool) const {}
-    GA_FN double cache_g(int) const { return 0.0; }
-    GA_FN double cache_h(int) const { return 0.0; }
-    GA_FN void cache_put_g(int, double) const {}
-    GA_FN void cache_put_h(int, double) const {}
     const double *H, *G, *L, *U;
     GA_FN double lo(int i) const { return L[i]; }
     GA_FN double hi(int i) const { return U[i]; }
@@ -695,7 +683,7 @@ const int* branch_overflow_counts(const DevNet& n, const DevState& s) {
 
 namespace {
 
-constexpr size_t kLaneSmem = static_cast<size_t>(kLaneFields) * kLaneBlock * sizeof(double);
+constexpr size_t kLaneSmem = static_cast<size_t>(kFields) * kLaneBlock * sizeof(double);
 
 struct Grids {
     int lane, tile, solo;

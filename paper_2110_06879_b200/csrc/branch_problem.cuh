@@ -37,10 +37,7 @@ enum Field : int {
     F_RHO = 32,   // 8 penalties
     F_LTIJ = 40, F_LTJI = 41, F_RHOT = 42,
     F_VMIN_I = 43, F_VMAX_I = 44, F_VMIN_J = 45, F_VMAX_J = 46, F_R2 = 47,
-    kFields = 48,
-    // lane phase with the gradient / Hessian cache: g (6) and H (36) of the
-    // last evaluated point
-    F_GC = 48, F_H = 54, kFieldsCache = 90
+    kFields = 48
 };
 
 // One branch's data: field f of slot s lives at smem[f * S + s].
@@ -161,23 +158,11 @@ struct YcView {
 };
 
 // The branch subproblem over a shared-memory slot (kernels.cpp:17-163).
-// kCache: the slot also keeps the gradient and Hessian of the last point
-// TRON evaluated them at; after a rejected step x is unchanged, so the next
-// step reloads them instead of re-evaluating (the evaluation is a pure
-// function of x and the slot's data: the same bits).
-template <int N, int S, bool kCache = false>
+template <int N, int S>
 struct BranchProb {
     static constexpr bool kLimited = N == 6;
-    static constexpr bool kGhCache = kCache;
     Slot<S> s;
     mutable double cc_, ss_;  // sincos at the last gradient point
-    mutable bool gh_valid_ = false;
-    __device__ __forceinline__ bool gh_cached() const { return kCache && gh_valid_; }
-    __device__ __forceinline__ void gh_set(bool v) const { gh_valid_ = v; }
-    __device__ __forceinline__ double cache_g(int i) const { return s(F_GC + i); }
-    __device__ __forceinline__ double cache_h(int k) const { return s(F_H + k); }
-    __device__ __forceinline__ void cache_put_g(int i, double v) const { s.set(F_GC + i, v); }
-    __device__ __forceinline__ void cache_put_h(int k, double v) const { s.set(F_H + k, v); }
 
     __device__ __forceinline__ double lo(int i) const {
         switch (i) {

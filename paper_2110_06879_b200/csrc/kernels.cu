@@ -179,10 +179,7 @@ __device__ __forceinline__ bool ge_solve(double* S, double* rhs, double* mu) {
 #define GA_BUS_BLOCK 128
 #endif
 constexpr int kBB = GA_BUS_BLOCK;  // buses (threads) per block
-#ifndef GA_BUS_STAGE
-#define GA_BUS_STAGE 16
-#endif
-constexpr int kStage = GA_BUS_STAGE * kBB;  // staged rows per block; the rest are read from global
+constexpr int kStage = 16 * kBB;  // staged rows per block (8 and 12 measured: no better); the rest read from global
 
 // largest slot with off[slot] <= p  (off[0] = 0 <= p < off[kBB])
 __device__ __forceinline__ int find_slot(const int* off, int p) {

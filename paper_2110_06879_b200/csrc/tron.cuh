@@ -215,74 +215,104 @@ GA_FN double boundary_tau(const double* s, const double* p, double delta) {
 // failure is PROVEN need not be evaluated: the first successful trial, and
 // hence s and every later bit, are unchanged.
 //
-// Proof.  Let P be the components that move (g_i != 0 and not pinned at the
-// bound g pushes against; pinned and g_i == 0 components give s_i = 0
-// exactly).  If no component of P clips at alpha_1 (checked with a margin),
-// none clips at any smaller alpha (x is inside its box and the clamp is
-// monotone), and for every k
-//   s_i = -alpha g_i + e_i,  |e_i| <= d_i = 4u(|x_i| + alpha |g_i|)
-// (rounding of alpha g_i, of x_i - alpha g_i and of the difference;
-// u = 2^-53).  Then with G = sum g_i^2, K = g'Hg over P,
-//   q(s) - mu0 g's = alpha(alpha K / 2 - (1 - mu0) G) + r,
-// where |r| collects the e terms and the rounding of the computed q, g's
-// and of this expression itself; |r| <= err(alpha) below, a polynomial in
-// alpha built from the absolute sums A1 = sum|g_i||x_i|, Hx = sum|g_i||h_ij||x_j|,
-// Kabs = sum|g_i||h_ij||g_j|, Xhx = sum|x_i||h_ij||x_j| with generous
-// constants.  main(alpha) > err(alpha) therefore implies the computed
-// q(s_k) > mu0 g's_k, i.e. trial k fails.  Returns the number of leading
-// trials k = 1, 2, ... so proven (at most 39: the last trial always runs,
-// its step is the result when every trial fails).
+// Proof for one trial alpha.  Component i is pinned (g_i == 0, or x_i at the
+// bound g_i pushes against: s_i = 0 exactly), clipped (x_i - alpha g_i beyond
+// the bound in g's direction by a rounding margin: the clamp returns the
+// bound, s_i = c_i = fl(bound - x_i) exactly) or moving (strictly inside by
+// the margin: s_i = -alpha g_i + e_i, |e_i| <= d_i = 4u(|x_i| + alpha|g_i|),
+// u = 2^-53, from the roundings of alpha g_i, x_i - alpha g_i and the
+// difference); anything else stops the screen.  With C / M the clipped /
+// moving sets,
+//   q(s) - mu0 g's = A0 + alpha A1 + alpha^2 A2 + r,
+//   A0 = (1 - mu0) g_C'c + c'H_CC c / 2,
+//   A1 = -(1 - mu0) g_M'g_M - (c'H_CM g_M + g_M'H_MC c) / 2,  A2 = g_M'H_MM g_M / 2,
+// where r collects the e terms, the rounding of the computed q and mu0 g's
+// (the reference's model() and dot()), and the rounding of evaluating this
+// polynomial; |r| <= E0 + alpha E1 + alpha^2 E2, built from absolute sums
+// with generous constants (below).  A0 + alpha A1 + alpha^2 A2 > E(alpha)
+// therefore implies the computed q(s_k) > mu0 g's_k: trial k fails.  The
+// coefficients change only when the clipped set does (at most N times).
+// Returns the number of leading trials k = 1, 2, ... so proven (at most 39:
+// the last trial always runs, its step is the result when every trial fails).
 template <int N, class HM>
 GA_FN int cauchy_skip(const double* x, const double* g, const HM& h, const double* l,
                       const double* u, double alpha0) {
-    constexpr double kU = 1.1102230246251565e-16;  // 2^-53
-    constexpr double kC = (8 * N + 64) * kU;       // first-order rounding constant
-    const double a1 = alpha0 * 0.5;                // largest alpha skipped
-    if (!(alpha0 >= 1e-100)) return 0;             // keep every product a normal number
-    double gm[N], xa[N], ga[N];
+    constexpr double kU = 1.1102230246251565e-16;      // 2^-53
+    constexpr double kC = (2 * N * N + 3 * N + 40) * kU;  // first-order rounding constant
+    constexpr double kC1 = 1.0 - kTronMu0;
+    if (!(alpha0 >= 1e-100)) return 0;                 // keep every product a normal number
+    unsigned live = 0;                                 // components that move or clip
+    double cl[N];                                      // the clipped step of each live component
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         const bool pinned = g[i] == 0.0 || (x[i] <= l[i] && g[i] > 0.0) || (x[i] >= u[i] && g[i] < 0.0);
-        gm[i] = pinned ? 0.0 : g[i];
         if (!pinned && !(fabs(g[i]) >= 1e-150)) return 0;
-        if (!pinned) {  // x_i - alpha g_i must stay inside [l_i, u_i] for alpha <= a1
-            const double t = x[i] - a1 * g[i];
-            const double m = 8.0 * kU * (fabs(x[i]) + fabs(a1 * g[i]) + fabs(l[i]) + fabs(u[i]));
-            if (!(t - l[i] > m && u[i] - t > m)) return 0;
-        }
-        xa[i] = fabs(x[i]);
-        ga[i] = fabs(gm[i]);
+        if (!pinned) live |= 1u << i;
+        cl[i] = g[i] > 0.0 ? l[i] - x[i] : u[i] - x[i];  // fl(bound - x_i): the reference's s_i
     }
-    double G = 0.0, K = 0.0, A1 = 0.0, Hx = 0.0, Kabs = 0.0, Xhx = 0.0;
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-        G += gm[i] * gm[i];
-        A1 += ga[i] * xa[i];
-        double hg = 0.0, hga = 0.0, hxa = 0.0;
-#pragma unroll
-        for (int j = 0; j < N; ++j) {
-            const double hij = h[i * N + j], ha = fabs(hij);
-            hg += hij * gm[j];
-            hga += ha * ga[j];
-            hxa += ha * xa[j];
-        }
-        K += gm[i] * hg;
-        Kabs += ga[i] * hga;
-        Hx += ga[i] * hxa + xa[i] * hga;  // both orders: the computed H need not be symmetric
-        Xhx += xa[i] * hxa;
-    }
-    if (!(K > 0.0) || !(Kabs >= 1e-250) || !sfinite(Kabs) || !sfinite(Xhx)) return 0;
-    const double c1 = 1.0 - kTronMu0;
+    unsigned prev = ~0u;
+    double A0 = 0.0, A1 = 0.0, A2 = 0.0, E0 = 0.0, E1 = 0.0, E2 = 0.0;
     double a = alpha0;
-    int k = 0;
-    for (; k < 39; ++k) {
+    for (int k = 0; k < 39; ++k) {
         a *= 0.5;  // alpha_{k+1}
-        const double main = a * (0.5 * a * K - c1 * G);
-        const double err = kC * (A1 + a * (G + Hx) + a * a * Kabs) +
-                           64.0 * kU * kU * (Xhx + 2.0 * a * Hx + a * a * Kabs);
-        if (!(main > 1.0625 * err)) break;
+        unsigned mv = 0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            if (!(live >> i & 1u)) continue;
+            const double t = x[i] - a * g[i];
+            const double m = 8.0 * kU * (fabs(x[i]) + fabs(a * g[i]) + fabs(l[i]) + fabs(u[i]));
+            if (t - l[i] > m && u[i] - t > m) mv |= 1u << i;
+            else if (!(g[i] > 0.0 ? l[i] - t > m : t - u[i] > m)) return k;  // at a bound: unproven
+        }
+        if (mv != prev) {  // coefficients of this clipped set
+            prev = mv;
+            double gc = 0.0, G = 0.0, ScS = 0.0, X = 0.0, K = 0.0;
+            double SgC = 0.0, SgX = 0.0, sHs = 0.0, sHg = 0.0, Kabs = 0.0, sHx = 0.0, gHx = 0.0,
+                   xHx = 0.0;
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                const bool im = mv >> i & 1u, ic = (live >> i & 1u) && !im;
+                if (!im && !ic) continue;
+                if (ic) { gc += g[i] * cl[i]; SgC += fabs(g[i] * cl[i]); }
+                if (im) { G += g[i] * g[i]; SgX += fabs(g[i]) * fabs(x[i]); }
+#pragma unroll
+                for (int j = 0; j < N; ++j) {
+                    const bool jm = mv >> j & 1u, jc = (live >> j & 1u) && !jm;
+                    if (!jm && !jc) continue;
+                    const double hij = h[i * N + j], ha = fabs(hij);
+                    if (ic && jc) { ScS += cl[i] * hij * cl[j]; sHs += fabs(cl[i]) * ha * fabs(cl[j]); }
+                    if (im && jm) {
+                        K += g[i] * hij * g[j];
+                        Kabs += fabs(g[i]) * ha * fabs(g[j]);
+                        gHx += fabs(g[i]) * ha * fabs(x[j]) + fabs(x[i]) * ha * fabs(g[j]);
+                        xHx += fabs(x[i]) * ha * fabs(x[j]);
+                    }
+                    if (ic && jm) {
+                        X += cl[i] * hij * g[j];
+                        sHg += fabs(cl[i]) * ha * fabs(g[j]);
+                        sHx += fabs(cl[i]) * ha * fabs(x[j]);
+                    }
+                    if (im && jc) {
+                        X += g[i] * hij * cl[j];
+                        sHg += fabs(g[i]) * ha * fabs(cl[j]);
+                        sHx += fabs(x[i]) * ha * fabs(cl[j]);
+                    }
+                }
+            }
+            A0 = kC1 * gc + 0.5 * ScS;
+            A1 = -(kC1 * G) - 0.5 * X;
+            A2 = 0.5 * K;
+            E0 = kC * (SgC + sHs) + 8.0 * kU * (SgX + sHx) + 64.0 * kU * kU * xHx;
+            E1 = kC * (G + sHg) + 8.0 * kU * gHx;
+            E2 = kC * Kabs;
+            if (!sfinite(E0 + E1 + E2) || !sfinite(A0) || !sfinite(A1) || !sfinite(A2)) return k;
+            if (Kabs != 0.0 && !(Kabs >= 1e-250)) return k;  // keep the quadratic term normal
+        }
+        const double main = A0 + a * (A1 + a * A2);
+        const double err = E0 + a * (E1 + a * E2);
+        if (!(main > 1.0625 * err)) return k;
     }
-    return k;
+    return 39;
 }
 
 // Cauchy point (tron.cpp:101-137).
@@ -340,7 +370,11 @@ GA_FN void cauchy_point(const double* x, const double* g, const HM& h,
         } else {
             if (cnt >= 40) return;
             if (cnt == 0) {  // trial 0 failed: jump over the proven failures
+#ifndef GA_NO_CAUCHY_SKIP
                 const int sk = cauchy_skip<N>(x, g, h, l, u, a);
+#else
+                const int sk = 0;
+#endif
                 GA_STAT_ADD(7, sk);
                 for (int j = 0; j < sk; ++j) a *= 0.5;
                 cnt += sk;
@@ -490,7 +524,6 @@ GA_FN bool tron_begin(const P& prob, TronState<N>& st) {
     st.f = prob.value(st.x);
     st.delta = 0.0;
     st.iter = 0;
-    if constexpr (P::kGhCache) prob.gh_set(false);
     return sfinite(st.f);
 }
 
@@ -573,7 +606,11 @@ struct TileSearch {
         const double alpha0 = smin(1.0, delta / gnorm);
         // backtracking trials k = 1..sk are proven failures (cauchy_skip):
         // the backtracking lanes start at k = sk + 1
+#ifndef GA_NO_CAUCHY_SKIP
         const int sk = cauchy_skip<N>(x, g, h, l, u, alpha0);
+#else
+        const int sk = 0;
+#endif
         double mys[N];
         // One trial site and one broadcast site (code size: this runs in a
         // persistent kernel whose hot loop must stay in the instruction cache).
@@ -674,31 +711,17 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
     for (int i = 0; i < N; ++i) { l[i] = prob.lo(i); u[i] = prob.hi(i); }
     GA_CLK_DECL
     double g[N];
+    prob.gradient(st.x, g);
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+        if (!sfinite(g[i])) return kStepError;
+    if (proj_grad_norm<N>(st.x, g, l, u) <= cfg.gtol) return kStepConverged;
+    GA_CLK(0);
     double h[N * N];
-    if (prob.gh_cached()) {  // rejected last step: x, hence g and H, unchanged
+    search.template hessian<N>(prob, st.x, h);
 #pragma unroll
-        for (int i = 0; i < N; ++i) g[i] = prob.cache_g(i);
-        if (proj_grad_norm<N>(st.x, g, l, u) <= cfg.gtol) return kStepConverged;
-#pragma unroll
-        for (int i = 0; i < N * N; ++i) h[i] = prob.cache_h(i);
-    } else {
-        prob.gradient(st.x, g);
-#pragma unroll
-        for (int i = 0; i < N; ++i)
-            if (!sfinite(g[i])) return kStepError;
-        if (proj_grad_norm<N>(st.x, g, l, u) <= cfg.gtol) return kStepConverged;
-        GA_CLK(0);
-        search.template hessian<N>(prob, st.x, h);
-#pragma unroll
-        for (int i = 0; i < N * N; ++i)
-            if (!sfinite(h[i])) return kStepError;
-        if constexpr (P::kGhCache) {
-#pragma unroll
-            for (int i = 0; i < N; ++i) prob.cache_put_g(i, g[i]);
-#pragma unroll
-            for (int i = 0; i < N * N; ++i) prob.cache_put_h(i, h[i]);
-        }
-    }
+    for (int i = 0; i < N * N; ++i)
+        if (!sfinite(h[i])) return kStepError;
     constexpr bool kOol = Search::kOolDivSqrt;
     if (st.iter == 0 && st.delta == 0.0) st.delta = smax(vnorm2<N, kOol>(g), cfg.delta_floor);
 
@@ -729,7 +752,6 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
     if (ratio < 0.25) st.delta = 0.25 * smax(snorm, 1e-12);
     else if (ratio > 0.75 && snorm >= 0.9 * st.delta) st.delta = smin(2.0 * st.delta, kTronDeltaMax);
     const bool accepted = ared > 0.0 && ratio > kTronEta;
-    if constexpr (P::kGhCache) prob.gh_set(!accepted);
     if (accepted) {
 #pragma unroll
         for (int i = 0; i < N; ++i) st.x[i] = xt[i];

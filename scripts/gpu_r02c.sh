@@ -7,12 +7,11 @@ timeout 2400 python -m pytest tests -m gpu -q --timeout=900 > $O/pytest_gpu.log 
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
 for v in stage8 stage12 ghc; do GRIDADMM_LIB=paper_2110_06879_b200/libgridadmm_$v.so timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-converge --no-track > $O/bench_$v.json 2>&1; done
 timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-converge --no-track > $O/bench_stage16.json 2>&1
+for v in ghc stage12; do GRIDADMM_LIB=paper_2110_06879_b200/libgridadmm_$v.so timeout 300 python scripts/converge_time.py > $O/conv_$v.json 2>&1; done
+timeout 300 python scripts/converge_time.py > $O/conv_default.json 2>&1
 GRIDADMM_LIB=paper_2110_06879_b200/libgridadmm_stats.so timeout 600 python scripts/probe_path_stats.py case_ACTIVSg70k case_ACTIVSg70k 5 20 > $O/stats_70k_5.json 2>&1
 GRIDADMM_LIB=paper_2110_06879_b200/libgridadmm_stats.so timeout 600 python scripts/probe_path_stats.py case_ACTIVSg70k case_ACTIVSg70k 3000 20 > $O/stats_70k_3000.json 2>&1
 timeout 600 python scripts/probe_solve_profile.py case_ACTIVSg70k case_ACTIVSg70k $O/solve_profile_70k.json > $O/solve_profile.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-converge --no-track > $O/launches.log 2>&1
 O=gpurun_out/c/ncu bash scripts/gpu_ncu.sh > gpurun_out/c/ncu.log 2>&1
-for tool in memcheck racecheck initcheck; do
-  timeout 900 compute-sanitizer --tool $tool --print-limit 50 python scripts/sanitize_target.py 2 > $O/sanitize_$tool.log 2>&1; echo "rc=$?" >> $O/sanitize_$tool.log
-done
 echo done

@@ -56,6 +56,10 @@ out = {"shape": shape, "periods": periods, "preset": preset, "ramp_frac": 0.02,
        "cpu_status": ga.STATUS[rst], "cpu_periods": len(rper), "cpu_wall_s": cpu_wall,
        "cpu_cores": workers, "cpu_cold_s": rtimes[0],
        "cpu_warm_s_per_step_mean": float(np.mean(cwarm)) if cwarm else None,
+       "gpu_warm_s_per_step_mean_same_periods": float(np.mean(gwarm[:len(cwarm)])) if cwarm else None,
+       "warm_speedup_same_periods": (float(np.mean(cwarm)) / float(np.mean(gwarm[:len(cwarm)]))
+                                     if cwarm else None),
+       "cpu_inner_per_period": [p.get("inner_iterations") for p in rper],
        "objectives_bit_identical": all(same), "periods_compared": len(same),
        "gpu_per_period": gper}
 print(json.dumps(out), flush=True)

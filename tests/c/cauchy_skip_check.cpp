@@ -107,7 +107,19 @@ long run(long count, std::mt19937_64& rng, long* skipped, long* trials) {
             const int z = pick(rng);
             g[i] = z == 0 ? 0.0 : gs * U(rng) * (z == 1 ? 1e-9 : 1.0);
         }
-        const double delta = scale(rng, -8, 4);
+        double delta = scale(rng, -8, 4);
+        if (pick(rng) < 3) {
+            // boundary stress: alpha0 = 1 (delta >= |g|) and some component
+            // reaching its bound exactly (to a few ulps) at a trial alpha 2^-k
+            const int i = pick(rng) % N;
+            const int k = 1 + pick(rng) * 2;
+            x[i] = l[i] + (u[i] - l[i]) * 0.25;
+            g[i] = std::ldexp(x[i] - l[i], k);
+            for (int r = pick(rng) % 4; r > 0; --r) g[i] = std::nextafter(g[i], pick(rng) < 5 ? 0.0 : 1e300);
+            double gn = 0.0;
+            for (int j = 0; j < N; ++j) gn += g[j] * g[j];
+            delta = 2.0 * std::sqrt(gn) + 1.0;
+        }
         double s1[N], s2[N], qs = 0.0;
         bool qok = false;
         long t0 = 0;

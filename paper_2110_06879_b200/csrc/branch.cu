@@ -209,6 +209,8 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
     unsigned my_exec = 0;  // trust-region steps executed by this lane
     const Slot<kLaneBlock> slot{smem + threadIdx.x};
     BranchProb<N, kLaneBlock> p{slot};
+    // the CG's Cholesky factor: a [k][lane] block after the slots
+    const SerialSearchT<kLaneBlock> search{smem + kFields * kLaneBlock + threadIdx.x};
     const TronParams tp = tron_params(cfg);
     const double kInf = __longlong_as_double(0x7ff0000000000000LL);
 
@@ -269,7 +271,7 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
         const int budget = active <= cfg.tile_slots ? cfg.lane_budget : cfg.lane_cap;
         if (b >= 0) {
             const int iter_before = ts.iter;
-            const int r = tron_step<N>(p, ts, tp);
+            const int r = tron_step<N>(p, ts, tp, search);
             ++my_exec;
             if (r != kStepContinue) {
                 const int status = solve_status<N, kLaneBlock, SerialSearch>(r, iter_before, p, ts,
@@ -683,7 +685,7 @@ const int* branch_overflow_counts(const DevNet& n, const DevState& s) {
 
 namespace {
 
-constexpr size_t kLaneSmem = static_cast<size_t>(kFields) * kLaneBlock * sizeof(double);
+constexpr size_t kLaneSmem = static_cast<size_t>(kFields + 36) * kLaneBlock * sizeof(double);
 
 struct Grids {
     int lane, tile, solo;

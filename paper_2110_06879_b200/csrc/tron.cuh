@@ -147,10 +147,29 @@ GA_FN double mdot(unsigned fm, const double* a, const double* b) {
     return s;
 }
 
+// Storage of the Cholesky factor: registers, or (lane phase) a strided
+// per-thread column of shared memory, element k at p[k * S] — the factor is
+// the largest live array of the CG section, and in registers it pushes the
+// one-branch-per-lane kernel into spills.  Same values either way.
+template <int N>
+struct RegMat {
+    double v[N * N];
+    GA_FN double operator[](int k) const { return v[k]; }
+    GA_FN void put(int k, double x) { v[k] = x; }
+};
+#if defined(__CUDACC__)
+template <int S>
+struct SmemMat {
+    double* p;
+    __device__ __forceinline__ double operator[](int k) const { return p[k * S]; }
+    __device__ __forceinline__ void put(int k, double x) const { p[k * S] = x; }
+};
+#endif
+
 // Cholesky of the free principal submatrix (tron.cpp:53-67): reads the lower
 // triangle h[i][j], i > j, as the reference's hf does.
-template <int N, bool kOol, class HM>
-GA_FN bool mcholesky(unsigned fm, const HM& h, double* L) {
+template <int N, bool kOol, class HM, class LM>
+GA_FN bool mcholesky(unsigned fm, const HM& h, LM& L) {
 #pragma unroll
     for (int j = 0; j < N; ++j) {
         if (!(fm >> j & 1u)) continue;
@@ -159,7 +178,7 @@ GA_FN bool mcholesky(unsigned fm, const HM& h, double* L) {
         for (int k = 0; k < j; ++k)
             if (fm >> k & 1u) d -= L[j * N + k] * L[j * N + k];
         if (d <= 0.0 || !sfinite(d)) return false;
-        L[j * N + j] = tsqrt<kOol>(d);
+        L.put(j * N + j, tsqrt<kOol>(d));
 #pragma unroll
         for (int i = j + 1; i < N; ++i) {
             if (!(fm >> i & 1u)) continue;
@@ -167,15 +186,15 @@ GA_FN bool mcholesky(unsigned fm, const HM& h, double* L) {
 #pragma unroll
             for (int k = 0; k < j; ++k)
                 if (fm >> k & 1u) v -= L[i * N + k] * L[j * N + k];
-            L[i * N + j] = tdiv<kOol>(v, L[j * N + j]);
+            L.put(i * N + j, tdiv<kOol>(v, L[j * N + j]));
         }
     }
     return true;
 }
 
 // (L L')^{-1} b on the free set (tron.cpp:69-80).
-template <int N, bool kOol>
-GA_FN void mchol_solve(unsigned fm, const double* L, const double* b, double* x) {
+template <int N, bool kOol, class LM>
+GA_FN void mchol_solve(unsigned fm, const LM& L, const double* b, double* x) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         if (!(fm >> i & 1u)) continue;
@@ -266,38 +285,44 @@ GA_FN int cauchy_skip(const double* x, const double* g, const HM& h, const doubl
         }
         if (mv != prev) {  // coefficients of this clipped set
             prev = mv;
+            double cs[N], gm[N], csa[N], gma[N], xma[N];
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                const bool im = mv >> i & 1u, ic = (live >> i & 1u) && !im;
+                cs[i] = ic ? cl[i] : 0.0;
+                gm[i] = im ? g[i] : 0.0;
+                csa[i] = fabs(cs[i]);
+                gma[i] = fabs(gm[i]);
+                xma[i] = im ? fabs(x[i]) : 0.0;
+            }
             double gc = 0.0, G = 0.0, ScS = 0.0, X = 0.0, K = 0.0;
             double SgC = 0.0, SgX = 0.0, sHs = 0.0, sHg = 0.0, Kabs = 0.0, sHx = 0.0, gHx = 0.0,
                    xHx = 0.0;
 #pragma unroll
             for (int i = 0; i < N; ++i) {
-                const bool im = mv >> i & 1u, ic = (live >> i & 1u) && !im;
-                if (!im && !ic) continue;
-                if (ic) { gc += g[i] * cl[i]; SgC += fabs(g[i] * cl[i]); }
-                if (im) { G += g[i] * g[i]; SgX += fabs(g[i]) * fabs(x[i]); }
+                double hc = 0.0, hg = 0.0, hac = 0.0, hag = 0.0, hax = 0.0;
 #pragma unroll
                 for (int j = 0; j < N; ++j) {
-                    const bool jm = mv >> j & 1u, jc = (live >> j & 1u) && !jm;
-                    if (!jm && !jc) continue;
                     const double hij = h[i * N + j], ha = fabs(hij);
-                    if (ic && jc) { ScS += cl[i] * hij * cl[j]; sHs += fabs(cl[i]) * ha * fabs(cl[j]); }
-                    if (im && jm) {
-                        K += g[i] * hij * g[j];
-                        Kabs += fabs(g[i]) * ha * fabs(g[j]);
-                        gHx += fabs(g[i]) * ha * fabs(x[j]) + fabs(x[i]) * ha * fabs(g[j]);
-                        xHx += fabs(x[i]) * ha * fabs(x[j]);
-                    }
-                    if (ic && jm) {
-                        X += cl[i] * hij * g[j];
-                        sHg += fabs(cl[i]) * ha * fabs(g[j]);
-                        sHx += fabs(cl[i]) * ha * fabs(x[j]);
-                    }
-                    if (im && jc) {
-                        X += g[i] * hij * cl[j];
-                        sHg += fabs(g[i]) * ha * fabs(cl[j]);
-                        sHx += fabs(x[i]) * ha * fabs(cl[j]);
-                    }
+                    hc += hij * cs[j];
+                    hg += hij * gm[j];
+                    hac += ha * csa[j];
+                    hag += ha * gma[j];
+                    hax += ha * xma[j];
                 }
+                gc += g[i] * cs[i];
+                SgC += fabs(g[i]) * csa[i];
+                G += gm[i] * gm[i];
+                SgX += gma[i] * xma[i];
+                ScS += cs[i] * hc;
+                X += cs[i] * hg + gm[i] * hc;
+                K += gm[i] * hg;
+                sHs += csa[i] * hac;
+                sHg += csa[i] * hag + gma[i] * hac;
+                Kabs += gma[i] * hag;
+                sHx += csa[i] * hax + xma[i] * hac;
+                gHx += gma[i] * hax + xma[i] * hag;
+                xHx += xma[i] * hax;
             }
             A0 = kC1 * gc + 0.5 * ScS;
             A1 = -(kC1 * G) - 0.5 * X;
@@ -388,10 +413,10 @@ GA_FN void cauchy_point(const double* x, const double* g, const HM& h,
 
 // Preconditioned Steihaug CG on the free subspace at x + s
 // (tron.cpp:141-224).  d receives the full-space correction.
-template <int N, bool kOol, class HM>
+template <int N, bool kOol, class HM, class Search>
 GA_FN void subspace_cg(const double* x, const double* g, const HM& h,
                        const double* l, const double* u, double delta,
-                       const TronParams& cfg, const double* s, double* d) {
+                       const TronParams& cfg, const double* s, double* d, const Search& search) {
 #pragma unroll
     for (int i = 0; i < N; ++i) d[i] = 0.0;
     unsigned fm = 0;
@@ -402,7 +427,8 @@ GA_FN void subspace_cg(const double* x, const double* g, const HM& h,
     }
     if (fm == 0) return;
 
-    double rf[N], L[N * N], zk[N], pk[N], dk[N];
+    double rf[N], zk[N], pk[N], dk[N];
+    auto L = search.template chol_mat<N>();
 #pragma unroll
     for (int i = 0; i < N; ++i) {  // rf = -(g + H s) on the free set
         double hs = 0.0;
@@ -530,9 +556,21 @@ GA_FN bool tron_begin(const P& prob, TronState<N>& st) {
 enum TronStep : int { kStepContinue = 0, kStepConverged = 1, kStepError = 2, kStepExhausted = 3 };
 
 // Sequential search strategy (one thread per solve): the reference's loops.
-struct SerialSearch {
+// S > 0: the Cholesky factor lives in shared memory at lbase[k * S].
+template <int S = 0>
+struct SerialSearchT {
     static constexpr bool kClocked = false;
     static constexpr bool kOolDivSqrt = true;
+    double* lbase = nullptr;
+    template <int N>
+    GA_FN auto chol_mat() const {
+#if defined(__CUDACC__)
+        if constexpr (S > 0) return SmemMat<S>{lbase};
+        else return RegMat<N>();
+#else
+        return RegMat<N>();
+#endif
+    }
     template <int N, class P>
     GA_FN void hessian(const P& prob, const double* x, double* h) const { prob.hessian(x, h); }
     template <int N, class HM>
@@ -563,6 +601,7 @@ struct SerialSearch {
         return qc;
     }
 };
+using SerialSearch = SerialSearchT<0>;
 
 #if defined(__CUDACC__)
 // Speculative search strategy for a tile of T lanes (power of two, <= 32)
@@ -579,6 +618,8 @@ struct TileSearch {
     static constexpr bool kOolDivSqrt = false;
     template <int N, class P>
     __device__ void hessian(const P& prob, const double* x, double* h) const { prob.hessian(x, h); }
+    template <int N>
+    __device__ RegMat<N> chol_mat() const { return RegMat<N>(); }
     unsigned mask;  // warp lanes of this tile
     int base;       // first warp lane of the tile
     int rank;       // lane within the tile
@@ -731,7 +772,7 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
     bool qs_ok = false;
     search.template cauchy<N>(st.x, g, h, l, u, st.delta, s, &qs, &qs_ok);
     GA_CLK(2);
-    subspace_cg<N, Search::kOolDivSqrt>(st.x, g, h, l, u, st.delta, cfg, s, d);
+    subspace_cg<N, Search::kOolDivSqrt>(st.x, g, h, l, u, st.delta, cfg, s, d, search);
     GA_CLK(3);
 
     const double qc = qs_ok ? qs : model<N>(g, h, s);

@@ -368,11 +368,12 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
     const int rank = lane & (T - 1);
     const int tbase = lane & ~(T - 1);
     const unsigned mask = (T == 32 ? 0xffffffffu : ((1u << T) - 1u)) << tbase;
-    const TileSearch<T> search{mask, tbase, rank};
     // A warp only ever uses the slots of its own 32 / kTile tiles, whatever T:
     // warps of one block may run different T (tail mode is decided per
     // queue), and must not share a slot.
-    const Slot<S> slot{smem + (threadIdx.x / T) * (T / kTile)};
+    const int si = (threadIdx.x / T) * (T / kTile);
+    const Slot<S> slot{smem + si};
+    const TileSearch<T> search{mask, tbase, rank, smem + kFields * S + 36 * si};
     BranchProb<N, S> p{slot};
     const TronParams tp = tron_params(cfg);
     const int count = *ovf_count;
@@ -450,7 +451,7 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
 __global__ void __launch_bounds__(kTileBlock, GA_TILE_MINB) tile_kernel(DevNet net, DevState st, BranchCfg cfg,
                                                           Work w, DevScalars* sc) {
     if (gate_closed(cfg)) return;
-    __shared__ double smem[kFields * (kTileBlock / kTile)];
+    __shared__ double smem[(kFields + 36) * (kTileBlock / kTile)];  // slots, then factors
     unsigned long long it6 = 0, it4 = 0;
     int fails = 0;
     // Tail mode: when a queue holds no more branches than half the grid's
@@ -502,7 +503,7 @@ __global__ void __launch_bounds__(kTileBlock, GA_TILE_MINB) tile_kernel(DevNet n
 __global__ void __launch_bounds__(kSoloBlock) solo_kernel(DevNet net, DevState st, BranchCfg cfg,
                                                           Work w, DevScalars* sc) {
     if (gate_closed(cfg)) return;
-    __shared__ double smem[kFields * (kTileBlock / kTile)];
+    __shared__ double smem[(kFields + 36) * (kTileBlock / kTile)];  // slots, then factors
     unsigned long long it6 = 0, it4 = 0;
     int fails = 0;
     tile_phase<6, 32>(net, st, cfg, w.solo6, &w.ctr[6], &w.ctr[8], smem, &it6, &fails, &sc->exec6, 0,
@@ -569,7 +570,8 @@ __global__ void tron_qp_kernel(int count, const double* H, const double* G, cons
     const int tbase = lane & ~(T - 1);
     const unsigned mask = (T == 32 ? 0xffffffffu : ((1u << T) - 1u)) << tbase;
     if (k >= count) return;
-    const TileSearch<T> search{mask, tbase, rank};
+    __shared__ double lsm[36 * (128 / T)];
+    const TileSearch<T> search{mask, tbase, rank, lsm + 36 * (threadIdx.x / T)};
     QpProb<N> p{H + (size_t)k * N * N, G + (size_t)k * N, L + (size_t)k * N, U + (size_t)k * N};
     TronParams tp;
     TronState<N> ts;

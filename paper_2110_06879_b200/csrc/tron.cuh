@@ -618,11 +618,15 @@ struct TileSearch {
     static constexpr bool kOolDivSqrt = false;
     template <int N, class P>
     __device__ void hessian(const P& prob, const double* x, double* h) const { prob.hessian(x, h); }
+    // The tile's Cholesky factor, one copy per tile in shared memory: every
+    // lane computes the same factor and writes each entry before reading
+    // it, so the identical values other lanes write are harmless.
     template <int N>
-    __device__ RegMat<N> chol_mat() const { return RegMat<N>(); }
+    __device__ SmemMat<1> chol_mat() const { return SmemMat<1>{lbase}; }
     unsigned mask;  // warp lanes of this tile
     int base;       // first warp lane of the tile
     int rank;       // lane within the tile
+    double* lbase;  // this tile's N x N factor in shared memory
 
     __device__ __forceinline__ unsigned ballot(bool p) const {
         return (__ballot_sync(mask, p) >> base) & ((T == 32) ? 0xffffffffu : ((1u << T) - 1u));

@@ -262,27 +262,35 @@ GA_FN int cauchy_skip(const double* x, const double* g, const HM& h, const doubl
     if (!(alpha0 >= 1e-100)) return 0;                 // keep every product a normal number
     unsigned live = 0;                                 // components that move or clip
     double cl[N];                                      // the clipped step of each live component
+    double ag[N], dmv[N], dcl[N];  // moving: alpha |g_i| < dmv_i; clipped: alpha |g_i| > dcl_i
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         const bool pinned = g[i] == 0.0 || (x[i] <= l[i] && g[i] > 0.0) || (x[i] >= u[i] && g[i] < 0.0);
         if (!pinned && !(fabs(g[i]) >= 1e-150)) return 0;
         if (!pinned) live |= 1u << i;
         cl[i] = g[i] > 0.0 ? l[i] - x[i] : u[i] - x[i];  // fl(bound - x_i): the reference's s_i
+        // distance to the bound g drives toward, and a rounding margin valid
+        // for every alpha <= alpha0 (the step rounds x_i - alpha g_i twice)
+        const double dist = g[i] > 0.0 ? x[i] - l[i] : u[i] - x[i];
+        ag[i] = fabs(g[i]);
+        const double m = 8.0 * kU * (fabs(x[i]) + alpha0 * ag[i] + fabs(l[i]) + fabs(u[i]));
+        dmv[i] = (dist - m) * (1.0 - 16.0 * kU);
+        dcl[i] = (dist + m) * (1.0 + 16.0 * kU);
     }
     unsigned prev = ~0u;
     double A0 = 0.0, A1 = 0.0, A2 = 0.0, E0 = 0.0, E1 = 0.0, E2 = 0.0;
     double a = alpha0;
     for (int k = 0; k < 39; ++k) {
         a *= 0.5;  // alpha_{k+1}
-        unsigned mv = 0;
+        unsigned mv = 0, amb = 0;
 #pragma unroll
         for (int i = 0; i < N; ++i) {
-            if (!(live >> i & 1u)) continue;
-            const double t = x[i] - a * g[i];
-            const double m = 8.0 * kU * (fabs(x[i]) + fabs(a * g[i]) + fabs(l[i]) + fabs(u[i]));
-            if (t - l[i] > m && u[i] - t > m) mv |= 1u << i;
-            else if (!(g[i] > 0.0 ? l[i] - t > m : t - u[i] > m)) return k;  // at a bound: unproven
+            const double step = a * ag[i];
+            mv |= (step < dmv[i] ? 1u : 0u) << i;
+            amb |= (!(step < dmv[i]) && !(step > dcl[i]) ? 1u : 0u) << i;
         }
+        mv &= live;
+        if (amb & live) return k;  // a component within the margin of its bound: unproven
         if (mv != prev) {  // coefficients of this clipped set
             prev = mv;
             double cs[N], gm[N], csa[N], gma[N], xma[N];

@@ -209,8 +209,6 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
     unsigned my_exec = 0;  // trust-region steps executed by this lane
     const Slot<kLaneBlock> slot{smem + threadIdx.x};
     BranchProb<N, kLaneBlock> p{slot};
-    // the CG's Cholesky factor: a [k][lane] block after the slots
-    const SerialSearchT<kLaneBlock> search{smem + kFields * kLaneBlock + threadIdx.x};
     const TronParams tp = tron_params(cfg);
     const double kInf = __longlong_as_double(0x7ff0000000000000LL);
 
@@ -271,7 +269,7 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
         const int budget = active <= cfg.tile_slots ? cfg.lane_budget : cfg.lane_cap;
         if (b >= 0) {
             const int iter_before = ts.iter;
-            const int r = tron_step<N>(p, ts, tp, search);
+            const int r = tron_step<N>(p, ts, tp);
             ++my_exec;
             if (r != kStepContinue) {
                 const int status = solve_status<N, kLaneBlock, SerialSearch>(r, iter_before, p, ts,
@@ -368,12 +366,11 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
     const int rank = lane & (T - 1);
     const int tbase = lane & ~(T - 1);
     const unsigned mask = (T == 32 ? 0xffffffffu : ((1u << T) - 1u)) << tbase;
+    const TileSearch<T> search{mask, tbase, rank};
     // A warp only ever uses the slots of its own 32 / kTile tiles, whatever T:
     // warps of one block may run different T (tail mode is decided per
     // queue), and must not share a slot.
-    const int si = (threadIdx.x / T) * (T / kTile);
-    const Slot<S> slot{smem + si};
-    const TileSearch<T> search{mask, tbase, rank, smem + kFields * S + 36 * si};
+    const Slot<S> slot{smem + (threadIdx.x / T) * (T / kTile)};
     BranchProb<N, S> p{slot};
     const TronParams tp = tron_params(cfg);
     const int count = *ovf_count;
@@ -451,7 +448,7 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
 __global__ void __launch_bounds__(kTileBlock, GA_TILE_MINB) tile_kernel(DevNet net, DevState st, BranchCfg cfg,
                                                           Work w, DevScalars* sc) {
     if (gate_closed(cfg)) return;
-    __shared__ double smem[(kFields + 36) * (kTileBlock / kTile)];  // slots, then factors
+    __shared__ double smem[kFields * (kTileBlock / kTile)];
     unsigned long long it6 = 0, it4 = 0;
     int fails = 0;
     // Tail mode: when a queue holds no more branches than half the grid's
@@ -503,7 +500,7 @@ __global__ void __launch_bounds__(kTileBlock, GA_TILE_MINB) tile_kernel(DevNet n
 __global__ void __launch_bounds__(kSoloBlock) solo_kernel(DevNet net, DevState st, BranchCfg cfg,
                                                           Work w, DevScalars* sc) {
     if (gate_closed(cfg)) return;
-    __shared__ double smem[(kFields + 36) * (kTileBlock / kTile)];  // slots, then factors
+    __shared__ double smem[kFields * (kTileBlock / kTile)];
     unsigned long long it6 = 0, it4 = 0;
     int fails = 0;
     tile_phase<6, 32>(net, st, cfg, w.solo6, &w.ctr[6], &w.ctr[8], smem, &it6, &fails, &sc->exec6, 0,
@@ -570,8 +567,7 @@ __global__ void tron_qp_kernel(int count, const double* H, const double* G, cons
     const int tbase = lane & ~(T - 1);
     const unsigned mask = (T == 32 ? 0xffffffffu : ((1u << T) - 1u)) << tbase;
     if (k >= count) return;
-    __shared__ double lsm[36 * (128 / T)];
-    const TileSearch<T> search{mask, tbase, rank, lsm + 36 * (threadIdx.x / T)};
+    const TileSearch<T> search{mask, tbase, rank};
     QpProb<N> p{H + (size_t)k * N * N, G + (size_t)k * N, L + (size_t)k * N, U + (size_t)k * N};
     TronParams tp;
     TronState<N> ts;
@@ -687,7 +683,7 @@ const int* branch_overflow_counts(const DevNet& n, const DevState& s) {
 
 namespace {
 
-constexpr size_t kLaneSmem = static_cast<size_t>(kFields + 36) * kLaneBlock * sizeof(double);
+constexpr size_t kLaneSmem = static_cast<size_t>(kFields) * kLaneBlock * sizeof(double);
 
 struct Grids {
     int lane, tile, solo;

@@ -25,18 +25,15 @@
 namespace ga {
 
 // Optional path statistics (debug builds with -DGA_TRON_STATS): TRON steps,
-// Cauchy extrapolations, Cauchy halvings evaluated, CG iterations,
-// line-search steps, failed Cholesky preconditioners / fixed points,
-// rejected steps, Cauchy halvings skipped by the pre-screen.
+// Cauchy extrapolations, Cauchy halvings, CG iterations, line-search
+// steps, failed Cholesky preconditioners.
 #ifdef GA_TRON_STATS
 __device__ unsigned long long g_tron_stats[8];  // tron.cuh is included by one TU
 #endif
 #if defined(GA_TRON_STATS) && defined(__CUDA_ARCH__)
 #define GA_STAT(k) atomicAdd(&g_tron_stats[k], 1ull)
-#define GA_STAT_ADD(k, v) atomicAdd(&g_tron_stats[k], (unsigned long long)(v))
 #else
 #define GA_STAT(k) ((void)0)
-#define GA_STAT_ADD(k, v) ((void)0)
 #endif
 
 // Optional section clocks (debug builds with -DGA_STEP_CLOCKS): cycles of
@@ -147,29 +144,10 @@ GA_FN double mdot(unsigned fm, const double* a, const double* b) {
     return s;
 }
 
-// Storage of the Cholesky factor: registers, or (lane phase) a strided
-// per-thread column of shared memory, element k at p[k * S] — the factor is
-// the largest live array of the CG section, and in registers it pushes the
-// one-branch-per-lane kernel into spills.  Same values either way.
-template <int N>
-struct RegMat {
-    double v[N * N];
-    GA_FN double operator[](int k) const { return v[k]; }
-    GA_FN void put(int k, double x) { v[k] = x; }
-};
-#if defined(__CUDACC__)
-template <int S>
-struct SmemMat {
-    double* p;
-    __device__ __forceinline__ double operator[](int k) const { return p[k * S]; }
-    __device__ __forceinline__ void put(int k, double x) const { p[k * S] = x; }
-};
-#endif
-
 // Cholesky of the free principal submatrix (tron.cpp:53-67): reads the lower
 // triangle h[i][j], i > j, as the reference's hf does.
-template <int N, bool kOol, class HM, class LM>
-GA_FN bool mcholesky(unsigned fm, const HM& h, LM& L) {
+template <int N, bool kOol, class HM>
+GA_FN bool mcholesky(unsigned fm, const HM& h, double* L) {
 #pragma unroll
     for (int j = 0; j < N; ++j) {
         if (!(fm >> j & 1u)) continue;
@@ -178,7 +156,7 @@ GA_FN bool mcholesky(unsigned fm, const HM& h, LM& L) {
         for (int k = 0; k < j; ++k)
             if (fm >> k & 1u) d -= L[j * N + k] * L[j * N + k];
         if (d <= 0.0 || !sfinite(d)) return false;
-        L.put(j * N + j, tsqrt<kOol>(d));
+        L[j * N + j] = tsqrt<kOol>(d);
 #pragma unroll
         for (int i = j + 1; i < N; ++i) {
             if (!(fm >> i & 1u)) continue;
@@ -186,15 +164,15 @@ GA_FN bool mcholesky(unsigned fm, const HM& h, LM& L) {
 #pragma unroll
             for (int k = 0; k < j; ++k)
                 if (fm >> k & 1u) v -= L[i * N + k] * L[j * N + k];
-            L.put(i * N + j, tdiv<kOol>(v, L[j * N + j]));
+            L[i * N + j] = tdiv<kOol>(v, L[j * N + j]);
         }
     }
     return true;
 }
 
 // (L L')^{-1} b on the free set (tron.cpp:69-80).
-template <int N, bool kOol, class LM>
-GA_FN void mchol_solve(unsigned fm, const LM& L, const double* b, double* x) {
+template <int N, bool kOol>
+GA_FN void mchol_solve(unsigned fm, const double* L, const double* b, double* x) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         if (!(fm >> i & 1u)) continue;
@@ -224,128 +202,6 @@ GA_FN double boundary_tau(const double* s, const double* p, double delta) {
     const double ss = vdot<N>(s, s);
     const double disc = smax(0.0, sp * sp + pp * (delta * delta - ss));
     return tdiv<kOol>(-sp + tsqrt<kOol>(disc), pp);
-}
-
-// ---- exact pre-screen of Cauchy backtracking trials ---------------------
-// The backtracking loop (tron.cpp:127-135) evaluates trials at
-// alpha_k = alpha0 * 2^-k, k = 1..40, and stops at the first k with
-//   ok(s_k) = ||s_k|| <= delta  &&  q(s_k) <= mu0 * g's_k,
-// s_k = clip(x - alpha_k g) - x.  Trials are independent, so a trial whose
-// failure is PROVEN need not be evaluated: the first successful trial, and
-// hence s and every later bit, are unchanged.
-//
-// Proof for one trial alpha.  Component i is pinned (g_i == 0, or x_i at the
-// bound g_i pushes against: s_i = 0 exactly), clipped (x_i - alpha g_i beyond
-// the bound in g's direction by a rounding margin: the clamp returns the
-// bound, s_i = c_i = fl(bound - x_i) exactly) or moving (strictly inside by
-// the margin: s_i = -alpha g_i + e_i, |e_i| <= d_i = 4u(|x_i| + alpha|g_i|),
-// u = 2^-53, from the roundings of alpha g_i, x_i - alpha g_i and the
-// difference); anything else stops the screen.  With C / M the clipped /
-// moving sets,
-//   q(s) - mu0 g's = A0 + alpha A1 + alpha^2 A2 + r,
-//   A0 = (1 - mu0) g_C'c + c'H_CC c / 2,
-//   A1 = -(1 - mu0) g_M'g_M - (c'H_CM g_M + g_M'H_MC c) / 2,  A2 = g_M'H_MM g_M / 2,
-// where r collects the e terms, the rounding of the computed q and mu0 g's
-// (the reference's model() and dot()), and the rounding of evaluating this
-// polynomial; |r| <= E0 + alpha E1 + alpha^2 E2, built from absolute sums
-// with generous constants (below).  A0 + alpha A1 + alpha^2 A2 > E(alpha)
-// therefore implies the computed q(s_k) > mu0 g's_k: trial k fails.  The
-// coefficients change only when the clipped set does (at most N times).
-// Returns the number of leading trials k = 1, 2, ... so proven (at most 39:
-// the last trial always runs, its step is the result when every trial fails).
-template <int N, class HM>
-GA_FN int cauchy_skip(const double* x, const double* g, const HM& h, const double* l,
-                      const double* u, double alpha0) {
-    constexpr double kU = 1.1102230246251565e-16;      // 2^-53
-    constexpr double kC = (2 * N * N + 3 * N + 40) * kU;  // first-order rounding constant
-    constexpr double kC1 = 1.0 - kTronMu0;
-    if (!(alpha0 >= 1e-100)) return 0;                 // keep every product a normal number
-    unsigned live = 0;                                 // components that move or clip
-    double cl[N];                                      // the clipped step of each live component
-    double ag[N], dmv[N], dcl[N];  // moving: alpha |g_i| < dmv_i; clipped: alpha |g_i| > dcl_i
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-        const bool pinned = g[i] == 0.0 || (x[i] <= l[i] && g[i] > 0.0) || (x[i] >= u[i] && g[i] < 0.0);
-        if (!pinned && !(fabs(g[i]) >= 1e-150)) return 0;
-        if (!pinned) live |= 1u << i;
-        cl[i] = g[i] > 0.0 ? l[i] - x[i] : u[i] - x[i];  // fl(bound - x_i): the reference's s_i
-        // distance to the bound g drives toward, and a rounding margin valid
-        // for every alpha <= alpha0 (the step rounds x_i - alpha g_i twice)
-        const double dist = g[i] > 0.0 ? x[i] - l[i] : u[i] - x[i];
-        ag[i] = fabs(g[i]);
-        const double m = 8.0 * kU * (fabs(x[i]) + alpha0 * ag[i] + fabs(l[i]) + fabs(u[i]));
-        dmv[i] = (dist - m) * (1.0 - 16.0 * kU);
-        dcl[i] = (dist + m) * (1.0 + 16.0 * kU);
-    }
-    unsigned prev = ~0u;
-    double A0 = 0.0, A1 = 0.0, A2 = 0.0, E0 = 0.0, E1 = 0.0, E2 = 0.0;
-    double a = alpha0;
-    for (int k = 0; k < 39; ++k) {
-        a *= 0.5;  // alpha_{k+1}
-        unsigned mv = 0, amb = 0;
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-            const double step = a * ag[i];
-            mv |= (step < dmv[i] ? 1u : 0u) << i;
-            amb |= (!(step < dmv[i]) && !(step > dcl[i]) ? 1u : 0u) << i;
-        }
-        mv &= live;
-        if (amb & live) return k;  // a component within the margin of its bound: unproven
-        if (mv != prev) {  // coefficients of this clipped set
-            prev = mv;
-            double cs[N], gm[N], csa[N], gma[N], xma[N];
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                const bool im = mv >> i & 1u, ic = (live >> i & 1u) && !im;
-                cs[i] = ic ? cl[i] : 0.0;
-                gm[i] = im ? g[i] : 0.0;
-                csa[i] = fabs(cs[i]);
-                gma[i] = fabs(gm[i]);
-                xma[i] = im ? fabs(x[i]) : 0.0;
-            }
-            double gc = 0.0, G = 0.0, ScS = 0.0, X = 0.0, K = 0.0;
-            double SgC = 0.0, SgX = 0.0, sHs = 0.0, sHg = 0.0, Kabs = 0.0, sHx = 0.0, gHx = 0.0,
-                   xHx = 0.0;
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                double hc = 0.0, hg = 0.0, hac = 0.0, hag = 0.0, hax = 0.0;
-#pragma unroll
-                for (int j = 0; j < N; ++j) {
-                    const double hij = h[i * N + j], ha = fabs(hij);
-                    hc += hij * cs[j];
-                    hg += hij * gm[j];
-                    hac += ha * csa[j];
-                    hag += ha * gma[j];
-                    hax += ha * xma[j];
-                }
-                gc += g[i] * cs[i];
-                SgC += fabs(g[i]) * csa[i];
-                G += gm[i] * gm[i];
-                SgX += gma[i] * xma[i];
-                ScS += cs[i] * hc;
-                X += cs[i] * hg + gm[i] * hc;
-                K += gm[i] * hg;
-                sHs += csa[i] * hac;
-                sHg += csa[i] * hag + gma[i] * hac;
-                Kabs += gma[i] * hag;
-                sHx += csa[i] * hax + xma[i] * hac;
-                gHx += gma[i] * hax + xma[i] * hag;
-                xHx += xma[i] * hax;
-            }
-            A0 = kC1 * gc + 0.5 * ScS;
-            A1 = -(kC1 * G) - 0.5 * X;
-            A2 = 0.5 * K;
-            E0 = kC * (SgC + sHs) + 8.0 * kU * (SgX + sHx) + 64.0 * kU * kU * xHx;
-            E1 = kC * (G + sHg) + 8.0 * kU * gHx;
-            E2 = kC * Kabs;
-            if (!sfinite(E0 + E1 + E2) || !sfinite(A0) || !sfinite(A1) || !sfinite(A2)) return k;
-            if (Kabs != 0.0 && !(Kabs >= 1e-250)) return k;  // keep the quadratic term normal
-        }
-        const double main = A0 + a * (A1 + a * A2);
-        const double err = E0 + a * (E1 + a * E2);
-        if (!(main > 1.0625 * err)) return k;
-    }
-    return 39;
 }
 
 // Cauchy point (tron.cpp:101-137).
@@ -402,16 +258,6 @@ GA_FN void cauchy_point(const double* x, const double* g, const HM& h,
             a = a * 2.0;
         } else {
             if (cnt >= 40) return;
-            if (cnt == 0) {  // trial 0 failed: jump over the proven failures
-#ifndef GA_NO_CAUCHY_SKIP
-                const int sk = cauchy_skip<N>(x, g, h, l, u, a);
-#else
-                const int sk = 0;
-#endif
-                GA_STAT_ADD(7, sk);
-                for (int j = 0; j < sk; ++j) a *= 0.5;
-                cnt += sk;
-            }
             GA_STAT(2);
             a *= 0.5;
         }
@@ -421,10 +267,10 @@ GA_FN void cauchy_point(const double* x, const double* g, const HM& h,
 
 // Preconditioned Steihaug CG on the free subspace at x + s
 // (tron.cpp:141-224).  d receives the full-space correction.
-template <int N, bool kOol, class HM, class Search>
+template <int N, bool kOol, class HM>
 GA_FN void subspace_cg(const double* x, const double* g, const HM& h,
                        const double* l, const double* u, double delta,
-                       const TronParams& cfg, const double* s, double* d, const Search& search) {
+                       const TronParams& cfg, const double* s, double* d) {
 #pragma unroll
     for (int i = 0; i < N; ++i) d[i] = 0.0;
     unsigned fm = 0;
@@ -435,8 +281,7 @@ GA_FN void subspace_cg(const double* x, const double* g, const HM& h,
     }
     if (fm == 0) return;
 
-    double rf[N], zk[N], pk[N], dk[N];
-    auto L = search.template chol_mat<N>();
+    double rf[N], L[N * N], zk[N], pk[N], dk[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {  // rf = -(g + H s) on the free set
         double hs = 0.0;
@@ -564,21 +409,9 @@ GA_FN bool tron_begin(const P& prob, TronState<N>& st) {
 enum TronStep : int { kStepContinue = 0, kStepConverged = 1, kStepError = 2, kStepExhausted = 3 };
 
 // Sequential search strategy (one thread per solve): the reference's loops.
-// S > 0: the Cholesky factor lives in shared memory at lbase[k * S].
-template <int S = 0>
-struct SerialSearchT {
+struct SerialSearch {
     static constexpr bool kClocked = false;
     static constexpr bool kOolDivSqrt = true;
-    double* lbase = nullptr;
-    template <int N>
-    GA_FN auto chol_mat() const {
-#if defined(__CUDACC__)
-        if constexpr (S > 0) return SmemMat<S>{lbase};
-        else return RegMat<N>();
-#else
-        return RegMat<N>();
-#endif
-    }
     template <int N, class P>
     GA_FN void hessian(const P& prob, const double* x, double* h) const { prob.hessian(x, h); }
     template <int N, class HM>
@@ -609,7 +442,6 @@ struct SerialSearchT {
         return qc;
     }
 };
-using SerialSearch = SerialSearchT<0>;
 
 #if defined(__CUDACC__)
 // Speculative search strategy for a tile of T lanes (power of two, <= 32)
@@ -626,15 +458,9 @@ struct TileSearch {
     static constexpr bool kOolDivSqrt = false;
     template <int N, class P>
     __device__ void hessian(const P& prob, const double* x, double* h) const { prob.hessian(x, h); }
-    // The tile's Cholesky factor, one copy per tile in shared memory: every
-    // lane computes the same factor and writes each entry before reading
-    // it, so the identical values other lanes write are harmless.
-    template <int N>
-    __device__ SmemMat<1> chol_mat() const { return SmemMat<1>{lbase}; }
     unsigned mask;  // warp lanes of this tile
     int base;       // first warp lane of the tile
     int rank;       // lane within the tile
-    double* lbase;  // this tile's N x N factor in shared memory
 
     __device__ __forceinline__ unsigned ballot(bool p) const {
         return (__ballot_sync(mask, p) >> base) & ((T == 32) ? 0xffffffffu : ((1u << T) - 1u));
@@ -657,26 +483,19 @@ struct TileSearch {
             return;
         }
         const double alpha0 = smin(1.0, delta / gnorm);
-        // backtracking trials k = 1..sk are proven failures (cauchy_skip):
-        // the backtracking lanes start at k = sk + 1
-#ifndef GA_NO_CAUCHY_SKIP
-        const int sk = cauchy_skip<N>(x, g, h, l, u, alpha0);
-#else
-        const int sk = 0;
-#endif
         double mys[N];
         // One trial site and one broadcast site (code size: this runs in a
         // persistent kernel whose hot loop must stay in the instruction cache).
         // Candidate exponents c (trial at alpha0 * 2^c):
-        //   round 0: rank 0 -> 0, rank 1 -> +1, ranks 2.. -> -(sk+1), -(sk+2), ...
+        //   round 0: rank 0 -> 0, rank 1 -> +1, ranks 2.. -> -1, -2, ...
         //   extrapolation rounds r >= 1: 2 + (r-1)*T + rank   (valid <= 20)
-        //   backtracking rounds r >= 1: -(sk + (T-1) + (r-1)*T + rank) (valid >= -40)
+        //   backtracking rounds r >= 1: -((T-1) + (r-1)*T + rank) (valid >= -40)
         int dir = 0;  // +1 extrapolating, -1 backtracking (decided in round 0)
         for (int round = 0;; ++round) {
             int c;
-            if (round == 0) c = rank == 0 ? 0 : (rank == 1 ? 1 : -(sk + rank - 1));
+            if (round == 0) c = rank == 0 ? 0 : (rank == 1 ? 1 : -(rank - 1));
             else if (dir > 0) c = 2 + (round - 1) * T + rank;
-            else c = -(sk + (T - 1) + (round - 1) * T + rank);
+            else c = -((T - 1) + (round - 1) * T + rank);
             const bool valid = dir > 0 ? c <= 20 : c >= -40;
             bool okc = false, mok = false;
             double mv = 0.0;
@@ -704,7 +523,6 @@ struct TileSearch {
                     dir = -1;
                     const unsigned hm = okm >> 2;
                     if (hm) src = __ffs(hm) - 1 + 2;
-                    else if (sk + T - 2 >= 40) src = 41 - sk;  // k = 40 was tried: its step
                     else done = false;
                 }
             } else if (dir > 0) {
@@ -712,7 +530,7 @@ struct TileSearch {
                 if (run > 0) src = run - 1;
                 done = run < T;  // a failure (or the c > 20 limit) ended the run
             } else {
-                const int kb = sk + (T - 1) + (round - 1) * T;  // this round tried k = kb..kb+T-1
+                const int kb = (T - 1) + (round - 1) * T;  // this round tried k = kb..kb+T-1
                 if (okm) src = __ffs(okm) - 1;
                 else if (kb + T - 1 >= 40) src = 40 - kb;  // none up to 2^-40: last trial's step
                 else done = false;
@@ -784,7 +602,7 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
     bool qs_ok = false;
     search.template cauchy<N>(st.x, g, h, l, u, st.delta, s, &qs, &qs_ok);
     GA_CLK(2);
-    subspace_cg<N, Search::kOolDivSqrt>(st.x, g, h, l, u, st.delta, cfg, s, d, search);
+    subspace_cg<N, Search::kOolDivSqrt>(st.x, g, h, l, u, st.delta, cfg, s, d);
     GA_CLK(3);
 
     const double qc = qs_ok ? qs : model<N>(g, h, s);
@@ -812,6 +630,7 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
     } else {
         GA_STAT(6);  // rejected step: x (hence g, H) unchanged
     }
+    if (st.iter >= 100) GA_STAT(7);  // steps of solves deep in the tail
     ++st.iter;
     // Fixed point: a rejected step that leaves the radius bit-identical
     // leaves the whole iterate (x, f, delta) unchanged, and an iteration with

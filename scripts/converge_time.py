@@ -15,11 +15,20 @@ shape = sys.argv[1] if len(sys.argv) > 1 else "case_ACTIVSg70k"
 preset = sys.argv[2] if len(sys.argv) > 2 else shape
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 net = ga.Network(synth.ensure_case(shape, "/tmp/gridadmm_cases"))
-ga.solve(net, ga.Config(preset, max_outer=1, max_inner=3))
+
+
+def config(**kw):
+    if ":" in preset:  # explicit "rho_pq:rho_va"
+        rpq, rva = (float(v) for v in preset.split(":"))
+        return ga.Config(rho_pq=rpq, rho_va=rva, **kw)
+    return ga.Config(preset, **kw)
+
+
+ga.solve(net, config(max_outer=1, max_inner=3))
 times = []
 for _ in range(reps):
     t0 = time.perf_counter()
-    st, rep = ga.solve(net, ga.Config(preset))
+    st, rep = ga.solve(net, config())
     times.append(time.perf_counter() - t0)
 m = rep.metrics()
 print(json.dumps({"lib": os.path.basename(ga.LIB_PATH), "shape": shape, "preset": preset,

@@ -179,7 +179,13 @@ __device__ __forceinline__ bool ge_solve(double* S, double* rhs, double* mu) {
 #define GA_BUS_BLOCK 128
 #endif
 constexpr int kBB = GA_BUS_BLOCK;  // buses (threads) per block
-constexpr int kStage = 16 * kBB;  // staged rows per block (8 and 12 measured: no better); the rest read from global
+#ifndef GA_BUS_STAGE
+#define GA_BUS_STAGE 16
+#endif
+#ifndef GA_BUS_MINB
+#define GA_BUS_MINB 1
+#endif
+constexpr int kStage = GA_BUS_STAGE * kBB;  // staged rows per block; the rest read from global
 
 // largest slot with off[slot] <= p  (off[0] = 0 <= p < off[kBB])
 __device__ __forceinline__ int find_slot(const int* off, int p) {
@@ -209,7 +215,7 @@ __device__ __forceinline__ unsigned long long global_ns() {
 }
 
 template <bool kZY>
-__global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, double beta,
+__global__ void __launch_bounds__(kBB, GA_BUS_MINB) bus_block_kernel(DevNet n, DevState s, double beta,
                                                        DevScalars* sc, LoopCtl* gate) {
     if (gate) {
         if (*reinterpret_cast<volatile int*>(&gate->stop)) return;

@@ -288,3 +288,19 @@ def test_device_metrics_with_line_limit_violation(gridadmm, oracle_mod, tmp_path
     assert mask_wall_clock_json(sol.read_text()) == mask_wall_clock_json(rsol.read_text())
     ref.h.gridadmm_report_free(rrep)
     ref.close()
+
+
+def test_full_solve_2868_shape_matches_reference(gridadmm, oracle_mod):
+    """Full cold start of the 2868rte-shaped synthetic grid (BASELINE
+    configs[1]) to convergence through both libraries' gridadmm_solve: status,
+    iteration counts and every metric bit (the reference on all host cores,
+    ~80 s on 16)."""
+    from gridcases import synth
+    path = synth.ensure_case("case2868rte", "/tmp/gridadmm_cases")
+    d = dict(rho_pq=1000.0, rho_va=1e4)
+    st, rep = gridadmm.solve(gridadmm.Network(path), gridadmm.Config(**d))
+    rst, rm = oracle_mod.capi_solve(oracle_mod.ref_capi(), path, workers=os.cpu_count() or 1, **d)
+    assert st == rst == 0
+    m = rep.metrics()
+    for k in rm:
+        assert bits(m[k]) == bits(rm[k]), (k, m[k], rm[k])

@@ -220,6 +220,7 @@ void Session::upload_network() {
     alloc(ds_.mig_iter, nl);
     alloc(ds_.mig_al, nl);
     alloc(ds_.mig_cost, nl);
+    alloc(ds_.order_tmp, std::max(lim.size(), unl.size()));
     if (plan_.parts > 1) {
         alloc(dn_.own_gens, plan_.gens.size()); put(dn_.own_gens, plan_.gens);
         alloc(dn_.own_buses, plan_.buses.size()); put(dn_.own_buses, plan_.buses);

@@ -683,38 +683,6 @@ const int* branch_overflow_counts(const DevNet& n, const DevState& s) {
 
 namespace {
 
-// Orders the two lane-phase queues by the branches' TRON iterations in the
-// previous sweep, most expensive first (a counting sort on min(cost, 255)):
-// a warp then takes branches of similar cost together.  The queue order
-// never changes a result (every branch's arithmetic is independent of where
-// it runs).  Block 0: rate-limited queue, block 1: unlimited.
-__global__ void __launch_bounds__(1024) order_by_cost_kernel(DevNet n, DevState s) {
-    __shared__ int hist[257];
-    int* list = blockIdx.x == 0 ? n.lim_list : n.unl_list;
-    const int count = blockIdx.x == 0 ? n.n_lim : n.n_unl;
-    for (int k = threadIdx.x; k < 257; k += blockDim.x) hist[k] = 0;
-    __syncthreads();
-    auto key = [&](int b) { const int c = s.br_cost[b]; return 255 - (c < 255 ? c : 255); };
-    for (int i = threadIdx.x; i < count; i += blockDim.x) atomicAdd(&hist[key(list[i])], 1);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int acc = 0;
-        for (int k = 0; k < 256; ++k) {
-            const int c = hist[k];
-            hist[k] = acc;
-            acc += c;
-        }
-    }
-    __syncthreads();
-    int* tmp = s.order_tmp;
-    for (int i = threadIdx.x; i < count; i += blockDim.x) {
-        const int b = list[i];
-        tmp[atomicAdd(&hist[key(b)], 1)] = b;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < count; i += blockDim.x) list[i] = tmp[i];
-}
-
 constexpr size_t kLaneSmem = static_cast<size_t>(kFields) * kLaneBlock * sizeof(double);
 
 struct Grids {
@@ -744,16 +712,6 @@ void launch_branches(const DevNet& n, const DevState& s, const BranchCfg& cfg, D
     if (n.nl <= 0) return;
     const Work w = work_of(n, s);
     cudaMemsetAsync(w.ctr, 0, kCounters * sizeof(int), st);
-#ifdef GA_ORDER_BY_COST
-    // (two queues share one scratch buffer: one block per queue, in turn)
-    order_by_cost_kernel<<<1, 1024, 0, st>>>(n, s);
-    {
-        DevNet n2 = n;
-        n2.lim_list = n.unl_list;
-        n2.n_lim = n.n_unl;
-        order_by_cost_kernel<<<1, 1024, 0, st>>>(n2, s);
-    }
-#endif
     const size_t lane_smem = kLaneSmem;
     const Grids& grids = branch_grids();
     const int lane_blocks = grids.lane, tile_blocks = grids.tile, solo_blocks = grids.solo;

@@ -73,7 +73,6 @@ struct DevState {
     int* mig_iter = nullptr;         // [nl] TRON iteration within the solve
     int* mig_al = nullptr;           // [nl] completed AL rounds
     int* mig_cost = nullptr;         // [nl] TRON iterations so far (stats)
-    int* order_tmp = nullptr;        // [max(n_lim, n_unl)] scratch of the queue ordering
 };
 
 struct DevNet;

@@ -70,16 +70,36 @@ __global__ void __launch_bounds__(kBlock) gen_kernel(DevNet n, DevState s) {
 }
 
 // The generator projection of one generator row (the expressions of
-// gen_kernel above), evaluated where the bus kernel consumes the row.
-__device__ __forceinline__ double gen_row_x(const DevNet& n, int row, double xb, double z, double y,
-                                            double rho) {
+// gen_kernel above), evaluated where the bus kernel consumes the row.  The
+// row's generator data are loaded first (GenRow) so the loads issue with the
+// row's state loads rather than after them.
+#ifdef GA_GEN_KERNEL
+constexpr bool kGenFused = false;  // A/B: the separate gen_kernel runs before the branches
+#else
+constexpr bool kGenFused = true;
+#endif
+struct GenRow {
+    double c1, c2, lo, hi;  // p row: c1, c2, pmin, pmax; q row: -, -, qmin, qmax
+};
+__device__ __forceinline__ GenRow load_gen_row(const DevNet& n, int row) {
     const int g = row >> 1;
+    GenRow r;
     if ((row & 1) == 0) {
-        const double p = (rho * (xb - z) - y - __ldg(n.g_c1 + g)) / (2.0 * __ldg(n.g_c2 + g) + rho);
-        return sclamp(p, __ldg(n.g_pmin + g), __ldg(n.g_pmax + g));
+        r.c1 = __ldg(n.g_c1 + g);
+        r.c2 = __ldg(n.g_c2 + g);
+        r.lo = __ldg(n.g_pmin + g);
+        r.hi = __ldg(n.g_pmax + g);
+    } else {
+        r.c1 = r.c2 = 0.0;
+        r.lo = __ldg(n.g_qmin + g);
+        r.hi = __ldg(n.g_qmax + g);
     }
-    const double q = (rho * (xb - z) - y) / rho;
-    return sclamp(q, __ldg(n.g_qmin + g), __ldg(n.g_qmax + g));
+    return r;
+}
+__device__ __forceinline__ double gen_row_x(int row, const GenRow& p, double xb, double z, double y,
+                                            double rho) {
+    if ((row & 1) == 0) return sclamp((rho * (xb - z) - y - p.c1) / (2.0 * p.c2 + rho), p.lo, p.hi);
+    return sclamp((rho * (xb - z) - y) / rho, p.lo, p.hi);
 }
 
 // ---- buses (kernels.cpp:294-413) ----------------------------------------
@@ -300,18 +320,22 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
             }
         }
         double q[kUnroll], xv[kUnroll], zv[kUnroll], yv[kUnroll];
+        GenRow gp[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
             if (row[u] >= 0) {
+                const bool gen = kGenFused && kZY && (g[u] == 2 || g[u] == 3);
                 q[u] = __ldg(s.rho + row[u]);
                 zv[u] = __ldg(s.z + row[u]);
                 yv[u] = __ldg(s.y + row[u]);
-                if (kZY && (g[u] == 2 || g[u] == 3))
-                    xv[u] = gen_row_x(n, row[u], __ldg(s.xbar + row[u]), zv[u], yv[u], q[u]);
-                else
-                    xv[u] = __ldg(s.x + row[u]);
+                xv[u] = __ldg((gen ? s.xbar : s.x) + row[u]);  // gen rows: the previous xbar
+                if (gen) gp[u] = load_gen_row(n, row[u]);
             }
         }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+            if (row[u] >= 0 && kGenFused && kZY && (g[u] == 2 || g[u] == 3))
+                xv[u] = gen_row_x(row[u], gp[u], xv[u], zv[u], yv[u], q[u]);
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
             if (row[u] < 0) continue;
@@ -340,8 +364,9 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
         auto raw = [&](int k, double* q, double* c) {
             const int row = rows[k];
             *q = s.rho[row];
-            const double xr = (kZY && k >= gl[2] && k < gl[4])
-                                  ? gen_row_x(n, row, s.xbar[row], s.z[row], s.y[row], *q)
+            const double xr = (kGenFused && kZY && k >= gl[2] && k < gl[4])
+                                  ? gen_row_x(row, load_gen_row(n, row), s.xbar[row], s.z[row],
+                                              s.y[row], *q)
                                   : s.x[row];
             *c = *q * (xr + s.z[row]) + s.y[row];
         };
@@ -459,6 +484,7 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
             }
         }
         double old[kUnroll], q[kUnroll], xv[kUnroll], zv[kUnroll], yv[kUnroll], lam[kUnroll];
+        GenRow gp[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
             if (row[u] >= 0) {
@@ -466,13 +492,16 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
                 q[u] = __ldg(s.rho + row[u]);
                 zv[u] = __ldg(s.z + row[u]);
                 yv[u] = __ldg(s.y + row[u]);
-                if (kZY && (g[u] == 2 || g[u] == 3)) {
-                    xv[u] = gen_row_x(n, row[u], old[u], zv[u], yv[u], q[u]);
-                    s.x[row[u]] = xv[u];
-                } else {
-                    xv[u] = __ldg(s.x + row[u]);
-                }
+                xv[u] = __ldg(s.x + row[u]);  // generator rows: replaced below
+                if (kGenFused && kZY && (g[u] == 2 || g[u] == 3)) gp[u] = load_gen_row(n, row[u]);
                 if (kZY) lam[u] = __ldg(s.lambda + row[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            if (row[u] >= 0 && kGenFused && kZY && (g[u] == 2 || g[u] == 3)) {
+                xv[u] = gen_row_x(row[u], gp[u], old[u], zv[u], yv[u], q[u]);
+                s.x[row[u]] = xv[u];
             }
         }
 #pragma unroll

@@ -190,7 +190,7 @@ int gridadmm_device_count(void);
  * f = g'x + x'Hx/2 of dimension n <= 6 (H row-major n*n per problem); x is
  * the start point in, solution out; status uses TronStatus numbering
  * (0 converged, 1 iteration limit, 2 numerical error).  tile = 1 runs one
- * solve per thread (lane phase), tile = 8 one solve per 8-lane tile with the
+ * solve per thread (lane phase), tile = 4, 8 or 32 one solve per tile with the
  * speculative Cauchy/line search (tile phase).  And the pinned device sincos
  * (ga_sincos.h) on n arguments. */
 gridadmm_status gridadmm_probe_tron_qp(int count, int n, const double* h,

@@ -485,7 +485,7 @@ def device_count() -> int:
 
 
 def probe_tron_qp(H, g, lo, hi, x0, tile: int = 1):
-    """Batched device TRON on dense box QPs; tile=1 lane mode, tile=8 tile mode."""
+    """Batched device TRON on dense box QPs; tile=1 lane mode, tile=4/8/32 tile modes."""
     count, n = g.shape
     x = np.ascontiguousarray(x0, dtype=np.float64).copy()
     status = np.zeros(count, dtype=np.int32)

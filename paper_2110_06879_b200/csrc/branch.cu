@@ -72,10 +72,8 @@ constexpr double kRhoTildeMax = 1e7;
 
 constexpr int kLaneBlock = 128;  // lane phase: one slot per thread
 constexpr int kTileBlock = 128;  // tile phase: one slot per tile
-#ifndef GA_TILE
-#define GA_TILE 8
-#endif
-constexpr int kTile = GA_TILE;   // lanes per branch in the tile phase
+constexpr int kTile = 4;  // lanes per branch in the tile phase (full 70k solve: 2 / 4 / 8 / 16
+                         // lanes -> 7.37 / 7.02 / 7.12 / 7.38 s)
 constexpr int kCounters = 12;
 constexpr int kSoloBlock = 32;  // solo phase: one warp per block, one branch per warp
 
@@ -740,7 +738,9 @@ void launch_tron_qp(int count, int n, const double* h, const double* g, const do
     const int blocks = (threads + 127) / 128;
 #define GA_QP(NN)                                                                                \
     case NN:                                                                                     \
-        if (tile == 8)                                                                           \
+        if (tile == 4)                                                                           \
+            tron_qp_kernel<NN, 4><<<blocks, 128, 0, st>>>(count, h, g, l, u, x, status, iterations); \
+        else if (tile == 8)                                                                      \
             tron_qp_kernel<NN, 8><<<blocks, 128, 0, st>>>(count, h, g, l, u, x, status, iterations); \
         else if (tile == 32)                                                                     \
             tron_qp_kernel<NN, 32><<<blocks, 128, 0, st>>>(count, h, g, l, u, x, status, iterations); \

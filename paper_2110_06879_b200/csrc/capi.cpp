@@ -591,7 +591,7 @@ int gridadmm_device_count(void) {
 gridadmm_status gridadmm_probe_tron_qp(int count, int n, const double* h, const double* g,
                                        const double* l, const double* u, double* x, int* status,
                                        int* iterations, int tile) {
-    if (count < 0 || n < 1 || n > 6 || (tile != 1 && tile != 8 && tile != 32))
+    if (count < 0 || n < 1 || n > 6 || (tile != 1 && tile != 4 && tile != 8 && tile != 32))
         return fail(GRIDADMM_ERR_INVALID_ARG, "bad qp batch");
     return guarded([&]() -> gridadmm_status {
         const size_t nn = static_cast<size_t>(count) * n;

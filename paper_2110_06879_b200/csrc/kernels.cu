@@ -73,11 +73,6 @@ __global__ void __launch_bounds__(kBlock) gen_kernel(DevNet n, DevState s) {
 // gen_kernel above), evaluated where the bus kernel consumes the row.  The
 // row's generator data are loaded first (GenRow) so the loads issue with the
 // row's state loads rather than after them.
-#ifdef GA_GEN_KERNEL
-constexpr bool kGenFused = false;  // A/B: the separate gen_kernel runs before the branches
-#else
-constexpr bool kGenFused = true;
-#endif
 struct GenRow {
     double c1, c2, lo, hi;  // p row: c1, c2, pmin, pmax; q row: -, -, qmin, qmax
 };
@@ -324,7 +319,7 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
             if (row[u] >= 0) {
-                const bool gen = kGenFused && kZY && (g[u] == 2 || g[u] == 3);
+                const bool gen = kZY && (g[u] == 2 || g[u] == 3);
                 q[u] = __ldg(s.rho + row[u]);
                 zv[u] = __ldg(s.z + row[u]);
                 yv[u] = __ldg(s.y + row[u]);
@@ -334,7 +329,7 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
         }
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u)
-            if (row[u] >= 0 && kGenFused && kZY && (g[u] == 2 || g[u] == 3))
+            if (row[u] >= 0 && kZY && (g[u] == 2 || g[u] == 3))
                 xv[u] = gen_row_x(row[u], gp[u], xv[u], zv[u], yv[u], q[u]);
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
@@ -364,7 +359,7 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
         auto raw = [&](int k, double* q, double* c) {
             const int row = rows[k];
             *q = s.rho[row];
-            const double xr = (kGenFused && kZY && k >= gl[2] && k < gl[4])
+            const double xr = (kZY && k >= gl[2] && k < gl[4])
                                   ? gen_row_x(row, load_gen_row(n, row), s.xbar[row], s.z[row],
                                               s.y[row], *q)
                                   : s.x[row];
@@ -493,13 +488,13 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
                 zv[u] = __ldg(s.z + row[u]);
                 yv[u] = __ldg(s.y + row[u]);
                 xv[u] = __ldg(s.x + row[u]);  // generator rows: replaced below
-                if (kGenFused && kZY && (g[u] == 2 || g[u] == 3)) gp[u] = load_gen_row(n, row[u]);
+                if (kZY && (g[u] == 2 || g[u] == 3)) gp[u] = load_gen_row(n, row[u]);
                 if (kZY) lam[u] = __ldg(s.lambda + row[u]);
             }
         }
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
-            if (row[u] >= 0 && kGenFused && kZY && (g[u] == 2 || g[u] == 3)) {
+            if (row[u] >= 0 && kZY && (g[u] == 2 || g[u] == 3)) {
                 xv[u] = gen_row_x(row[u], gp[u], old[u], zv[u], yv[u], q[u]);
                 s.x[row[u]] = xv[u];
             }

@@ -373,9 +373,6 @@ bool Session::inner_loop(const SolverConfig& cfg, int outer, double rho_max, dou
         prepare_branch_launch();
         check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture begin");
         for (int k = 0; k < kGraphIters; ++k) {
-#ifdef GA_GEN_KERNEL
-            launch_generators(dn_, ds_, stream_);
-#endif
             launch_branches(dn_, ds_, bc, sc_, stream_);
             launch_bus_zy(dn_, ds_, beta_, sc_, stream_, ctl_);
             launch_loop_control(ctl_, rec_, sc_, stream_);
@@ -587,9 +584,6 @@ int Session::iterate_ev(double out[4], PhaseTimes* times, cudaEvent_t end_event)
     launch_reset_scalars(sc_, stream_);
     cudaEventRecord(ev_[0], stream_);
     // the generator projection runs inside the bus kernel (kernels.cu)
-#ifdef GA_GEN_KERNEL
-    launch_generators(dn_, ds_, stream_);
-#endif
     cudaEventRecord(ev_[1], stream_);
     launch_branches(dn_, ds_, branch_cfg(cfg_), sc_, stream_, ev_[5]);
     cudaEventRecord(ev_[2], stream_);
@@ -642,9 +636,6 @@ int Session::iterate_ev(double out[4], PhaseTimes* times, cudaEvent_t end_event)
 void Session::enqueue_x_phase() {
     check(cudaSetDevice(cfg_.device), "cudaSetDevice");
     launch_reset_scalars(sc_, stream_);
-#ifdef GA_GEN_KERNEL
-    launch_generators(dn_, ds_, stream_);
-#endif
     launch_branches(dn_, ds_, branch_cfg(cfg_), sc_, stream_);  // generators: in the bus kernel
     check(cudaGetLastError(), "x phase launch");
 }

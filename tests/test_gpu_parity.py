@@ -62,12 +62,12 @@ def test_device_sincos_matches_host_shim(gridadmm, oracle_mod):
     assert_bits_equal(cd, ch, "cos")
 
 
-@pytest.mark.parametrize("tile", [1, 8, 32])
+@pytest.mark.parametrize("tile", [1, 4, 8, 32])
 @pytest.mark.parametrize("n", [4, 6, 2])
 def test_tron_core_matches_reference(gridadmm, oracle_mod, n, tile):
     """Batched device TRON vs reference solve_one on random box QPs (convex and
     indefinite), acceptance.cpp:458-520 style, in both the one-lane (serial
-    search), the 8-lane tile and the whole-warp (speculative search) formulations."""
+    search), the 4- and 8-lane tiles and the whole-warp (speculative search) formulations."""
     rng = np.random.default_rng(100 + n)
     count = 4000
     A = rng.normal(size=(count, n, n))

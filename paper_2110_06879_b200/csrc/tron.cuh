@@ -32,10 +32,8 @@ __device__ unsigned long long g_tron_stats[8];  // tron.cuh is included by one T
 #endif
 #if defined(GA_TRON_STATS) && defined(__CUDA_ARCH__)
 #define GA_STAT(k) atomicAdd(&g_tron_stats[k], 1ull)
-#define GA_STAT_ADD(k, v) atomicAdd(&g_tron_stats[k], (unsigned long long)(v))
 #else
 #define GA_STAT(k) ((void)0)
-#define GA_STAT_ADD(k, v) ((void)0)
 #endif
 
 // Optional section clocks (debug builds with -DGA_STEP_CLOCKS): cycles of
@@ -206,138 +204,6 @@ GA_FN double boundary_tau(const double* s, const double* p, double delta) {
     return tdiv<kOol>(-sp + tsqrt<kOol>(disc), pp);
 }
 
-// ---- exact pre-screen of Cauchy backtracking trials ---------------------
-// The backtracking loop (tron.cpp:127-135) evaluates trials at
-// alpha_k = alpha0 * 2^-k, k = 1..40, and stops at the first k with
-//   ok(s_k) = ||s_k|| <= delta  &&  q(s_k) <= mu0 * g's_k,
-// s_k = clip(x - alpha_k g) - x.  Trials are independent, so a trial whose
-// failure is PROVEN need not be evaluated: the first successful trial, and
-// hence s and every later bit, are unchanged.
-//
-// Proof for one trial alpha.  Component i is pinned (g_i == 0, or x_i at the
-// bound g_i pushes against: s_i = 0 exactly), clipped (x_i - alpha g_i beyond
-// the bound in g's direction by a rounding margin: the clamp returns the
-// bound, s_i = c_i = fl(bound - x_i) exactly) or moving (strictly inside by
-// the margin: s_i = -alpha g_i + e_i, |e_i| <= d_i = 4u(|x_i| + alpha|g_i|),
-// u = 2^-53, from the roundings of alpha g_i, x_i - alpha g_i and the
-// difference); anything else stops the screen.  With C / M the clipped /
-// moving sets,
-//   q(s) - mu0 g's = A0 + alpha A1 + alpha^2 A2 + r,
-//   A0 = (1 - mu0) g_C'c + c'H_CC c / 2,
-//   A1 = -(1 - mu0) g_M'g_M - (c'H_CM g_M + g_M'H_MC c) / 2,  A2 = g_M'H_MM g_M / 2,
-// where r collects the e terms, the rounding of the computed q and mu0 g's
-// (the reference's model() and dot()), and the rounding of evaluating this
-// polynomial; |r| <= E0 + alpha E1 + alpha^2 E2, built from absolute sums
-// with generous constants (below).  A0 + alpha A1 + alpha^2 A2 > E(alpha)
-// therefore implies the computed q(s_k) > mu0 g's_k: trial k fails.  The
-// coefficients change only when the clipped set does: as alpha halves, a
-// clipped component can only become moving, so the screen runs in at most
-// N + 1 segments, computing the coefficients once per segment; per trial
-// it evaluates two quadratics and re-checks the clipped components.
-// SIMT cost model: one branch per lane in the lane phase, so the screen is
-// used there only (tile searches already evaluate 8 / 32 trials per round).
-// Returns the number of leading trials k = 1, 2, ... so proven (at most 39:
-// the last trial always runs, its step is the result when every trial fails).
-template <int N, class HM>
-GA_FN int cauchy_skip(const double* x, const double* g, const HM& h, const double* l,
-                      const double* u, double alpha0) {
-    constexpr double kU = 1.1102230246251565e-16;         // 2^-53
-    constexpr double kC = (2 * N * N + 3 * N + 40) * kU;  // first-order rounding constant
-    constexpr double kC1 = 1.0 - kTronMu0;
-    if (!(alpha0 >= 1e-100)) return 0;                    // keep every product a normal number
-    unsigned live = 0;                                    // components that move or clip
-    double cl[N];                                         // the clipped step (the reference's s_i)
-    double ag[N], dmv[N], dcl[N];  // moving: alpha |g_i| < dmv_i; clipped: alpha |g_i| > dcl_i
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-        const bool pinned = g[i] == 0.0 || (x[i] <= l[i] && g[i] > 0.0) || (x[i] >= u[i] && g[i] < 0.0);
-        if (!pinned && !(fabs(g[i]) >= 1e-150)) return 0;
-        if (!pinned) live |= 1u << i;
-        cl[i] = g[i] > 0.0 ? l[i] - x[i] : u[i] - x[i];
-        // distance to the bound g drives toward, and a rounding margin valid
-        // for every alpha <= alpha0 (the step rounds x_i - alpha g_i twice)
-        const double dist = g[i] > 0.0 ? x[i] - l[i] : u[i] - x[i];
-        ag[i] = fabs(g[i]);
-        const double m = 8.0 * kU * (fabs(x[i]) + alpha0 * ag[i] + fabs(l[i]) + fabs(u[i]));
-        dmv[i] = (dist - m) * (1.0 - 16.0 * kU);
-        dcl[i] = (dist + m) * (1.0 + 16.0 * kU);
-    }
-    double a = alpha0 * 0.5;  // alpha of trial k + 1
-    int k = 0;                // trials proven so far
-    for (int seg = 0; seg <= N; ++seg) {
-        unsigned mv = 0, amb = 0;
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-            const double step = a * ag[i];
-            mv |= (step < dmv[i] ? 1u : 0u) << i;
-            amb |= (!(step < dmv[i]) && !(step > dcl[i]) ? 1u : 0u) << i;
-        }
-        mv &= live;
-        if (amb & live) return k;  // a component within the margin of its bound: unproven
-        const unsigned clip = live & ~mv;
-        double cs[N], gm[N], csa[N], gma[N], xma[N];
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-            const bool im = mv >> i & 1u, ic = clip >> i & 1u;
-            cs[i] = ic ? cl[i] : 0.0;
-            gm[i] = im ? g[i] : 0.0;
-            csa[i] = fabs(cs[i]);
-            gma[i] = fabs(gm[i]);
-            xma[i] = im ? fabs(x[i]) : 0.0;
-        }
-        double gc = 0.0, G = 0.0, ScS = 0.0, X = 0.0, K = 0.0;
-        double SgC = 0.0, SgX = 0.0, sHs = 0.0, sHg = 0.0, Kabs = 0.0, sHx = 0.0, gHx = 0.0,
-               xHx = 0.0;
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-            double hc = 0.0, hg = 0.0, hac = 0.0, hag = 0.0, hax = 0.0;
-#pragma unroll
-            for (int j = 0; j < N; ++j) {
-                const double hij = h[i * N + j], ha = fabs(hij);
-                hc += hij * cs[j];
-                hg += hij * gm[j];
-                hac += ha * csa[j];
-                hag += ha * gma[j];
-                hax += ha * xma[j];
-            }
-            gc += g[i] * cs[i];
-            SgC += fabs(g[i]) * csa[i];
-            G += gm[i] * gm[i];
-            SgX += gma[i] * xma[i];
-            ScS += cs[i] * hc;
-            X += cs[i] * hg + gm[i] * hc;
-            K += gm[i] * hg;
-            sHs += csa[i] * hac;
-            sHg += csa[i] * hag + gma[i] * hac;
-            Kabs += gma[i] * hag;
-            sHx += csa[i] * hax + xma[i] * hac;
-            gHx += gma[i] * hax + xma[i] * hag;
-            xHx += xma[i] * hax;
-        }
-        const double A0 = kC1 * gc + 0.5 * ScS;
-        const double A1 = -(kC1 * G) - 0.5 * X;
-        const double A2 = 0.5 * K;
-        const double E0 = kC * (SgC + sHs) + 8.0 * kU * (SgX + sHx) + 64.0 * kU * kU * xHx;
-        const double E1 = kC * (G + sHg) + 8.0 * kU * gHx;
-        const double E2 = kC * Kabs;
-        if (!sfinite(E0 + E1 + E2) || !sfinite(A0) || !sfinite(A1) || !sfinite(A2)) return k;
-        if (Kabs != 0.0 && !(Kabs >= 1e-250)) return k;  // keep the quadratic term normal
-        for (;;) {  // the trials of this segment
-            const double main = A0 + a * (A1 + a * A2);
-            const double err = E0 + a * (E1 + a * E2);
-            if (!(main > 1.0625 * err)) return k;
-            if (++k >= 39) return 39;
-            a *= 0.5;
-            bool same = true;  // every clipped component still clipped (moving ones stay moving)
-#pragma unroll
-            for (int i = 0; i < N; ++i)
-                if (clip >> i & 1u) same = same && a * ag[i] > dcl[i];
-            if (!same) break;
-        }
-    }
-    return k;
-}
-
 // Cauchy point (tron.cpp:101-137).
 template <int N, bool kOol, class HM>
 GA_FN void cauchy_point(const double* x, const double* g, const HM& h,
@@ -392,16 +258,6 @@ GA_FN void cauchy_point(const double* x, const double* g, const HM& h,
             a = a * 2.0;
         } else {
             if (cnt >= 40) return;
-            if (cnt == 0) {  // trial 0 failed: jump over the proven failures
-#ifndef GA_NO_CAUCHY_SKIP
-                const int sk = cauchy_skip<N>(x, g, h, l, u, a);
-#else
-                const int sk = 0;  // A/B only
-#endif
-                GA_STAT_ADD(7, sk);
-                for (int j = 0; j < sk; ++j) a *= 0.5;
-                cnt += sk;
-            }
             GA_STAT(2);
             a *= 0.5;
         }
@@ -774,6 +630,7 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
     } else {
         GA_STAT(6);  // rejected step: x (hence g, H) unchanged
     }
+    if (st.iter >= 100) GA_STAT(7);  // steps of solves deep in the tail
     ++st.iter;
     // Fixed point: a rejected step that leaves the radius bit-identical
     // leaves the whole iterate (x, f, delta) unchanged, and an iteration with

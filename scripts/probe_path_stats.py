@@ -23,7 +23,7 @@ s.iterate(window)
 ga.lib().gridadmm_debug_tron_stats(buf, 1)
 c1 = s.step_counters()
 names = ["steps", "cauchy_extrapolations", "cauchy_halvings", "cg_iterations", "line_search_trials",
-         "chol_fail_or_fixed_point", "rejected_steps", "cauchy_halvings_skipped"]
+         "chol_fail_or_fixed_point", "rejected_steps", "steps_iter_ge_100"]
 st = dict(zip(names, list(buf)))
 steps = max(1, st["steps"])
 out = {"shape": shape, "preset": preset, "window": [warm, warm + window - 1],

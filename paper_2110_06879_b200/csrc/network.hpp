@@ -76,6 +76,27 @@ struct BusCsr {
 };
 BusCsr build_bus_csr(const Network& net);
 
+// Device storage order of the m coupling rows ("bus-major quads"): bus i
+// owns one contiguous segment [seg, end) holding its generators' (p, q) row
+// pairs in generator order, then — from a 4-aligned qstart — one quad
+// (p, q, w, theta) per incident branch end in branch order: the rows
+// (pij, qij, wi, thi) of a branch at its from-bus, (pji, qji, wj, thj) at its
+// to-bus.  Each reference group (decomp.cpp:13-30) is then a strided walk
+// in the reference's push order, so every ordered sum is unchanged, while
+// the bus phase reads its rows contiguously and a branch reads two 32-byte
+// quads.  Segments start on a multiple of 4; the gap after the generator
+// pairs is padding (positions with no row, rid = -1, whose state stays 0).
+struct RowLayout {
+    int mpad = 0;                  // storage positions (>= m)
+    std::vector<int> seg;          // 3 * nb: start, qstart, end
+    std::vector<int> gpos;         // ng: position of the generator's p row (q at +1)
+    std::vector<int> qpos;         // 2 * nl: from-quad, to-quad position of each branch
+    std::vector<int> rid;          // mpad: reference row id of each position, -1 = padding
+    std::vector<int> pos;          // m: position of each reference row
+    std::vector<int> quad_branch;  // mpad / 4: 2 b + side of the quad at 4 q, -1 otherwise
+};
+RowLayout build_row_layout(const Network& net);
+
 }  // namespace ga
 
 #endif

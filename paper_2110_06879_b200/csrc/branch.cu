@@ -172,11 +172,13 @@ __device__ __forceinline__ void finalize_branch(const DevNet& net, const DevStat
     }
     double fl[4];
     branch_flows(YcView<S>{slot}, pt[0], pt[1], pt[2], pt[3], fl);
-    double2* xr = reinterpret_cast<double2*>(st.x + 2 * net.ng + 8 * b);
-    xr[0] = make_double2(fl[0], fl[1]);
-    xr[1] = make_double2(fl[2], fl[3]);
-    xr[2] = make_double2(pt[0] * pt[0], pt[2]);
-    xr[3] = make_double2(pt[1] * pt[1], pt[3]);
+    // the from-quad (pij, qij, wi, thi) and the to-quad (pji, qji, wj, thj)
+    double2* xf = reinterpret_cast<double2*>(st.x + net.qpos[2 * b]);
+    double2* xt = reinterpret_cast<double2*>(st.x + net.qpos[2 * b + 1]);
+    xf[0] = make_double2(fl[0], fl[1]);
+    xt[0] = make_double2(fl[2], fl[3]);
+    xf[1] = make_double2(pt[0] * pt[0], pt[2]);
+    xt[1] = make_double2(pt[1] * pt[1], pt[3]);
 #if defined(GA_TRON_STATS) || defined(GA_BRANCH_STEPS)
     (void)iters;  // stats builds: br_cost = executed steps (+2^20 if the tile phase ran it)
 #else
@@ -598,18 +600,23 @@ __global__ void tron_qp_kernel(int count, const double* H, const double* G, cons
 // buses (w, theta).  Every x / xbar row is written by exactly one item.
 __global__ void cold_start_kernel(DevNet n, DevState s, double rho_pq, double rho_va,
                                   double limit_tighten) {
-    const long long total = (long long)n.m + n.nl + n.ng + n.nb;
+    const long long total = (long long)n.mpad + n.nl + n.ng + n.nb;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
          t += (long long)gridDim.x * blockDim.x) {
-        if (t < n.m) {
-            const int k = (int)t;
+        if (t < n.mpad) {
+            const int p = (int)t;
+            const int k = n.rid[p];  // reference row, -1 = padding (all zeros)
             const bool pq = k < 2 * n.ng || (k - 2 * n.ng) % 8 < 4;
-            s.z[k] = 0.0;
-            s.y[k] = 0.0;
-            s.lambda[k] = 0.0;
-            s.rho[k] = pq ? rho_pq : rho_va;
-        } else if (t < (long long)n.m + n.nl) {
-            const int b = (int)(t - n.m);
+            s.z[p] = 0.0;
+            s.y[p] = 0.0;
+            s.lambda[p] = 0.0;
+            s.rho[p] = k < 0 ? 0.0 : (pq ? rho_pq : rho_va);
+            if (k < 0) {
+                s.x[p] = 0.0;
+                s.xbar[p] = 0.0;
+            }
+        } else if (t < (long long)n.mpad + n.nl) {
+            const int b = (int)(t - n.mpad);
             const int from = n.br_from[b], to = n.br_to[b];
             const double vi = 0.5 * (n.b_vmin[from] + n.b_vmax[from]);
             const double vj = 0.5 * (n.b_vmin[to] + n.b_vmax[to]);
@@ -617,11 +624,12 @@ __global__ void cold_start_kernel(DevNet n, DevState s, double rho_pq, double rh
             double f[4];
             bp::branch_flows(yc, vi, vj, 0.0, 0.0, f);
             const double vals[8] = {f[0], f[1], f[2], f[3], vi * vi, 0.0, vj * vj, 0.0};
-            const int base = 2 * n.ng + 8 * b;
+            const int qf = n.qpos[2 * b], qt = n.qpos[2 * b + 1];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-                s.x[base + k] = vals[k];
-                s.xbar[base + k] = vals[k];
+                const int r = bp::branch_row_pos(qf, qt, k);
+                s.x[r] = vals[k];
+                s.xbar[r] = vals[k];
             }
             double sij = 0.0, sji = 0.0;
             const double rate = n.br_rate[b];
@@ -636,16 +644,17 @@ __global__ void cold_start_kernel(DevNet n, DevState s, double rho_pq, double rh
             s.lt_ij[b] = 0.0;
             s.lt_ji[b] = 0.0;
             s.rho_t[b] = rho_pq;
-        } else if (t < (long long)n.m + n.nl + n.ng) {
-            const int g = (int)(t - n.m - n.nl);
+        } else if (t < (long long)n.mpad + n.nl + n.ng) {
+            const int g = (int)(t - n.mpad - n.nl);
             const double p = 0.5 * (n.g_pmin[g] + n.g_pmax[g]);
             const double q = 0.5 * (n.g_qmin[g] + n.g_qmax[g]);
-            s.x[2 * g] = p;
-            s.xbar[2 * g] = p;
-            s.x[2 * g + 1] = q;
-            s.xbar[2 * g + 1] = q;
+            const int r = n.gpos[g];
+            s.x[r] = p;
+            s.xbar[r] = p;
+            s.x[r + 1] = q;
+            s.xbar[r + 1] = q;
         } else {
-            const int i = (int)(t - n.m - n.nl - n.ng);
+            const int i = (int)(t - n.mpad - n.nl - n.ng);
             const double v = 0.5 * (n.b_vmin[i] + n.b_vmax[i]);
             s.bus_w[i] = v * v;
             s.bus_theta[i] = 0.0;
@@ -756,7 +765,7 @@ void launch_tron_qp(int count, int n, const double* h, const double* g, const do
 
 void launch_cold_start(const DevNet& n, const DevState& s, double rho_pq, double rho_va,
                        double limit_tighten, cudaStream_t st) {
-    const long long total = (long long)n.m + n.nl + n.ng + n.nb;
+    const long long total = (long long)n.mpad + n.nl + n.ng + n.nb;
     if (total <= 0) return;
     long long blocks = (total + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;

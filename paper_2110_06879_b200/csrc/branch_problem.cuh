@@ -333,6 +333,12 @@ GA_FN void branch_flows(const Y& yc, double vi, double vj, double thi, double th
     out[3] = -yc(7) * wj - yc(5) * wr - yc(4) * wim;    // qji
 }
 
+// Storage position of branch row k (reference order pij, qij, pji, qji, wi,
+// thi, wj, thj) given the branch's from-quad qf and to-quad qt (device.hpp).
+__host__ __device__ __forceinline__ int branch_row_pos(int qf, int qt, int k) {
+    return (((k >> 1) & 1) ? qt : qf) + (k & 1) + ((k >> 2) << 1);
+}
+
 // Fills a slot for branch b (kernels.cpp:229-241).
 template <int S>
 __device__ __forceinline__ void load_slot(const DevNet& net, const DevState& st,
@@ -340,13 +346,14 @@ __device__ __forceinline__ void load_slot(const DevNet& net, const DevState& st,
     const int from = net.br_from[b], to = net.br_to[b];
 #pragma unroll
     for (int k = 0; k < 8; ++k) s.set(F_YC + k, __ldg(&net.br_y[k * net.nl + b]));
-    const int base = 2 * net.ng + 8 * b;
+    const int qf = __ldg(&net.qpos[2 * b]), qt = __ldg(&net.qpos[2 * b + 1]);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-        s.set(F_TGT + k, st.xbar[base + k]);
-        s.set(F_Y + k, st.y[base + k]);
-        s.set(F_Z + k, st.z[base + k]);
-        s.set(F_RHO + k, st.rho[base + k]);
+        const int r = branch_row_pos(qf, qt, k);
+        s.set(F_TGT + k, st.xbar[r]);
+        s.set(F_Y + k, st.y[r]);
+        s.set(F_Z + k, st.z[r]);
+        s.set(F_RHO + k, st.rho[r]);
     }
     s.set(F_LTIJ, st.lt_ij[b]);
     s.set(F_LTJI, st.lt_ji[b]);

@@ -2,17 +2,18 @@
 // extern "C"-style launchers the host driver calls (one per phase).
 //
 // Layout (all FP64 unless noted, SoA, 256-B aligned allocations):
-//   rows   m = 2G + 8L in the reference's CouplingLayout order
-//          (proj/src/decomp.hpp:32-36): gen g -> rows 2g, 2g+1; branch b ->
-//          rows 2G + 8b + k, k in (pij, qij, pji, qji, wi, thi, wj, thj).
-//          x, xbar, z, y, lambda, rho: 6 m-vectors.
+//   rows   the m = 2G + 8L coupling rows of the reference's CouplingLayout
+//          (proj/src/decomp.hpp:32-36) stored bus-major (network.hpp
+//          RowLayout): bus i owns the contiguous positions
+//          [seg, gen_end) generator (p, q) pairs in generator order,
+//          [gen_end, qstart) padding to a multiple of 4,
+//          [qstart, end) one quad (p, q, w, theta) per incident branch end in
+//          branch order.  x, xbar, z, y, lambda, rho: 6 mpad-vectors; the
+//          padding positions hold zeros forever.  gpos / qpos map
+//          generators / branch ends to positions.
 //   branch L: ends (int32 from/to), 8 admittance coefficients [k*L + b],
 //          rate, point [k*L + b] (k < 6), lt_ij, lt_ji, rho_tilde.
-//   bus    N: pd, qd, gs, bs, vmin, vmax, w, theta; a CSR of the m rows by
-//          owning bus, each bus's rows grouped as
-//          [w | theta | gen_p | gen_q | flow_p | flow_q] in the reference's
-//          per-group order (proj/src/decomp.cpp:7-31); grp[7*i + k] are the
-//          group start offsets (k = 0..6, last = end).
+//   bus    N: pd, qd, gs, bs, vmin, vmax, w, theta; segment bounds.
 //   gen    G: pmin, pmax, qmin, qmax, c2, c1.
 #ifndef GA_DEVICE_HPP
 #define GA_DEVICE_HPP
@@ -25,6 +26,7 @@ namespace ga {
 
 struct DevNet {
     int nb = 0, ng = 0, nl = 0, m = 0;
+    int mpad = 0;  // storage positions of the row vectors (m rows + padding)
     int ref_bus = -1;
     // generators
     double *g_pmin = nullptr, *g_pmax = nullptr, *g_qmin = nullptr, *g_qmax = nullptr;
@@ -39,8 +41,11 @@ struct DevNet {
     // buses
     double *b_pd = nullptr, *b_qd = nullptr, *b_gs = nullptr, *b_bs = nullptr;
     double *b_vmin = nullptr, *b_vmax = nullptr;
-    int* bus_grp = nullptr;   // [7*nb] group offsets into bus_rows
-    int* bus_rows = nullptr;  // [m]
+    int* bus_seg = nullptr;   // [4*nb] start, gen_end, qstart, end of each bus's rows
+    int* gpos = nullptr;      // [ng] position of generator g's p row (q row at +1)
+    int* qpos = nullptr;      // [2*nl] from-quad and to-quad position of branch b
+    int* quad_branch = nullptr;  // [mpad/4 + 1] 2 b + side of the quad at 4 q, else -1
+    int* rid = nullptr;       // [mpad] reference row of each position, -1 = padding
     // ownership subset of a multi-part run (partition.hpp); nullptr = all.
     // lim_list / unl_list above already hold only the owned branches.
     int* own_gens = nullptr;
@@ -50,7 +55,7 @@ struct DevNet {
 
     __host__ __device__ int gens_count() const { return own_gens ? n_own_gens : ng; }
     __host__ __device__ int buses_count() const { return own_buses ? n_own_buses : nb; }
-    __host__ __device__ int rows_count() const { return own_rows ? n_own_rows : m; }
+    __host__ __device__ int rows_count() const { return own_rows ? n_own_rows : mpad; }
     __host__ __device__ int gen_at(int t) const { return own_gens ? own_gens[t] : t; }
     __host__ __device__ int bus_at(int t) const { return own_buses ? own_buses[t] : t; }
     __host__ __device__ int row_at(int t) const { return own_rows ? own_rows[t] : t; }
@@ -106,6 +111,7 @@ struct DevExtract {
     double* vm = nullptr;     // [nb]
     double* va = nullptr;     // [nb]
     int* cand = nullptr;      // [nl] line-limit candidates (unordered)
+    double* gen_pq = nullptr; // [2 * ng] dispatch (pg, qg) in generator order
     ExtractScalars* sc = nullptr;
 };
 

@@ -10,9 +10,9 @@
 //  * ext_bus_kernel, one thread per bus and per generator: vm / va, the
 //    power-balance residuals pbal / qbal accumulated in the reference's
 //    order (driver.cpp:93-117: load and shunt, then generators in index
-//    order, then branch ends in branch order — exactly the bus's gen_p /
-//    flow_p row groups of the coupling CSR), and the voltage / generator
-//    bound violations.
+//    order, then branch ends in branch order — exactly the bus's segment of
+//    the row storage, device.hpp), the voltage / generator bound violations,
+//    and the dispatch in generator order.
 // The infinity norms and bound maxima are order-free maxima (NaN skipped as
 // std::max does), reduced as IEEE bit patterns of max(0, v): bit-identical
 // to the reference.  Two pieces stay on the host, both exact: the objective
@@ -83,24 +83,27 @@ __global__ void __launch_bounds__(kExtBlock) ext_bus_kernel(DevNet n, DevState s
         const double w = vm * vm;
         double pb = -n.b_pd[i] - n.b_gs[i] * w;
         double qb = -n.b_qd[i] + n.b_bs[i] * w;
-        const int* grp = n.bus_grp + 7 * i;  // [w | theta | gen_p | gen_q | flow_p | flow_q]
-        for (int k = grp[2]; k < grp[3]; ++k) pb += s.x[n.bus_rows[k]];
-        for (int k = grp[3]; k < grp[4]; ++k) qb += s.x[n.bus_rows[k]];
-        const int base = 2 * n.ng;
-        for (int k = grp[4]; k < grp[5]; ++k) {  // pij (k = 0) or pji (k = 2) rows, branch order
-            const int r = n.bus_rows[k] - base;
-            pb -= e.flows[4 * static_cast<size_t>(r >> 3) + (r & 7)];
+        // the bus's segment (device.hpp): generator (p, q) pairs in generator
+        // order, then one quad per incident branch end in branch order
+        const int* seg = n.bus_seg + 4 * i;
+        for (int k = seg[0]; k < seg[1]; k += 2) pb += s.x[k];
+        for (int k = seg[0] + 1; k < seg[1]; k += 2) qb += s.x[k];
+        for (int k = seg[2]; k < seg[3]; k += 4) {  // pij / pji, branch order
+            const int qb2 = n.quad_branch[k >> 2];  // 2 b + side
+            pb -= e.flows[4 * static_cast<size_t>(qb2 >> 1) + 2 * (qb2 & 1)];
         }
-        for (int k = grp[5]; k < grp[6]; ++k) {  // qij (1) or qji (3)
-            const int r = n.bus_rows[k] - base;
-            qb -= e.flows[4 * static_cast<size_t>(r >> 3) + (r & 7)];
+        for (int k = seg[2]; k < seg[3]; k += 4) {  // qij / qji
+            const int qb2 = n.quad_branch[k >> 2];
+            qb -= e.flows[4 * static_cast<size_t>(qb2 >> 1) + 2 * (qb2 & 1) + 1];
         }
         bal = fmax(fabs(pb), fabs(qb));
         bound = fmax(fmax(n.b_vmin[i] - vm, vm - n.b_vmax[i]), fabs(va) - kTwoPi);
     }
     if (t < n.ng) {
         const int g = t;
-        const double pg = s.x[2 * g], qg = s.x[2 * g + 1];
+        const double pg = s.x[n.gpos[g]], qg = s.x[n.gpos[g] + 1];
+        e.gen_pq[2 * g] = pg;
+        e.gen_pq[2 * g + 1] = qg;
         const double gv = fmax(fmax(n.g_pmin[g] - pg, pg - n.g_pmax[g]),
                                fmax(n.g_qmin[g] - qg, qg - n.g_qmax[g]));
         bound = fmax(bound, gv);

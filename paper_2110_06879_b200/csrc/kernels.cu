@@ -56,17 +56,18 @@ __global__ void __launch_bounds__(kBlock) gen_kernel(DevNet n, DevState s) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n.gens_count()) return;
     const int g = n.gen_at(t);
-    // rows 2g, 2g+1 are adjacent: one 16-B load per array
-    const double2 xb = reinterpret_cast<const double2*>(s.xbar)[g];
-    const double2 zz = reinterpret_cast<const double2*>(s.z)[g];
-    const double2 yy = reinterpret_cast<const double2*>(s.y)[g];
-    const double2 rr = reinterpret_cast<const double2*>(s.rho)[g];
+    // the p and q rows are adjacent (an even position): one 16-B load per array
+    const int h = n.gpos[g] >> 1;
+    const double2 xb = reinterpret_cast<const double2*>(s.xbar)[h];
+    const double2 zz = reinterpret_cast<const double2*>(s.z)[h];
+    const double2 yy = reinterpret_cast<const double2*>(s.y)[h];
+    const double2 rr = reinterpret_cast<const double2*>(s.rho)[h];
     const double p = (rr.x * (xb.x - zz.x) - yy.x - n.g_c1[g]) / (2.0 * n.g_c2[g] + rr.x);
     const double q = (rr.y * (xb.y - zz.y) - yy.y) / rr.y;
     double2 out;
     out.x = sclamp(p, n.g_pmin[g], n.g_pmax[g]);
     out.y = sclamp(q, n.g_qmin[g], n.g_qmax[g]);
-    reinterpret_cast<double2*>(s.x)[g] = out;
+    reinterpret_cast<double2*>(s.x)[h] = out;
 }
 
 // The generator projection of one generator row (the expressions of
@@ -209,12 +210,14 @@ __device__ __forceinline__ int find_slot(const int* off, int p) {
     return lo;
 }
 
-// column group of local row k: 0 w, 1 theta, 2 gen_p, 3 gen_q, 4 flow_p, 5 flow_q
-__device__ __forceinline__ int group_of(const int* gl, int k) {
-    int g = 0;
-#pragma unroll
-    for (int j = 1; j < 6; ++j) g += k >= gl[j] ? 1 : 0;
-    return g;
+// Column group of the local position k of a bus's segment (device.hpp):
+// 0 w, 1 theta, 2 gen_p, 3 gen_q, 4 flow_p, 5 flow_q, 6 padding.  ge / qs:
+// local end of the generator pairs / start of the quads.
+__device__ __forceinline__ int group_of(int ge, int qs, int k) {
+    if (k < ge) return 2 + (k & 1);
+    if (k < qs) return 6;
+    constexpr unsigned kQuadGroups = 4u | 5u << 4 | 0u << 8 | 1u << 12;  // p, q, w, theta
+    return (kQuadGroups >> (4 * ((k - qs) & 3))) & 15u;
 }
 
 constexpr int kFlagNonfinite = 1, kFlagSingular = 2, kFlagRef = 4;
@@ -234,8 +237,8 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
         if (blockIdx.x == 0 && threadIdx.x == 0) gate->t_bus = global_ns();
     }
     __shared__ int s_off[kBB + 1];
-    __shared__ int s_base[kBB];
-    __shared__ int s_gl[kBB][8];  // local group offsets 0..6, [7] = flags
+    __shared__ int s_base[kBB];       // segment start (storage position) of each slot's bus
+    __shared__ int s_gl[kBB][4];      // local gen end, quad start, count, flags
     __shared__ double s_res[kBB][5];  // mu0..2, w, theta
     __shared__ double s_a[kStage], s_b[kStage];
     __shared__ unsigned short s_pos[kStage];  // staged position -> slot << 3 | group
@@ -243,24 +246,24 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int t = blockIdx.x * kBB + tid;
     const int nbus = n.buses_count();
-    int i = -1, cnt = 0;
-    int gl[7] = {0, 0, 0, 0, 0, 0, 0};
+    int i = -1, cnt = 0, ge = 0, qs = 0;
     {
-        int g0 = 0;
+        int start = 0;
         if (t < nbus) {
             i = n.bus_at(t);
-            const int* grp = n.bus_grp + 7 * i;
-            g0 = __ldg(grp);
-#pragma unroll
-            for (int k = 1; k < 7; ++k) gl[k] = __ldg(grp + k) - g0;
-            cnt = gl[6];
+            const int* seg = n.bus_seg + 4 * i;
+            start = __ldg(seg);
+            ge = __ldg(seg + 1) - start;
+            qs = __ldg(seg + 2) - start;
+            cnt = __ldg(seg + 3) - start;
         }
-        s_base[tid] = g0;
-#pragma unroll
-        for (int k = 0; k < 7; ++k) s_gl[tid][k] = gl[k];
-        s_gl[tid][7] = (i >= 0 && i == n.ref_bus) ? kFlagRef : 0;
+        s_base[tid] = start;
+        s_gl[tid][0] = ge;
+        s_gl[tid][1] = qs;
+        s_gl[tid][2] = cnt;
+        s_gl[tid][3] = (i >= 0 && i == n.ref_bus) ? kFlagRef : 0;
     }
-    // block exclusive scan of the row counts
+    // block exclusive scan of the segment lengths
     int incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -275,32 +278,28 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
     const int my_off = woff + incl - cnt;
     s_off[tid] = my_off;
     if (tid == kBB - 1) s_off[kBB] = woff + incl;
-    // position map of this bus's staged rows
-    {
-        int g = 0;
-        for (int k = 0; k < cnt && my_off + k < kStage; ++k) {
-            while (g < 5 && k >= gl[g + 1]) ++g;
-            s_pos[my_off + k] = static_cast<unsigned short>(tid << 3 | g);
-        }
-    }
+    for (int k = 0; k < cnt && my_off + k < kStage; ++k)  // position map of the staged rows
+        s_pos[my_off + k] = static_cast<unsigned short>(tid << 3 | group_of(ge, qs, k));
     __syncthreads();
     const int total = s_off[kBB];
     const int staged = total < kStage ? total : kStage;
-    // (slot, local row, group) of position p
+    // (slot, local position, group) of block position p
     auto locate = [&](int p, int* slot, int* k, int* g) {
         if (p < kStage) {
             const int v = s_pos[p];
             *slot = v >> 3;
+            *k = p - s_off[*slot];
             *g = v & 7;
         } else {
             *slot = find_slot(s_off, p);
-            *g = -1;
+            *k = p - s_off[*slot];
+            *g = group_of(s_gl[*slot][0], s_gl[*slot][1], *k);
         }
-        *k = p - s_off[*slot];
-        if (*g < 0) *g = group_of(s_gl[*slot], *k);
     };
 
     // 1. gather: kUnroll positions per thread per trip, loads issued together
+    // (for one block of consecutive buses the positions are one contiguous
+    // range of the row vectors: coalesced)
     constexpr int kUnroll = 4;
     for (int p0 = tid; p0 < staged; p0 += kBB * kUnroll) {
         int row[kUnroll], slot[kUnroll], g[kUnroll];
@@ -311,7 +310,7 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
             if (p < staged) {
                 int k;
                 locate(p, &slot[u], &k, &g[u]);
-                row[u] = __ldg(n.bus_rows + s_base[slot[u]] + k);
+                if (g[u] != 6) row[u] = s_base[slot[u]] + k;
             }
         }
         double q[kUnroll], xv[kUnroll], zv[kUnroll], yv[kUnroll];
@@ -324,13 +323,13 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
                 zv[u] = __ldg(s.z + row[u]);
                 yv[u] = __ldg(s.y + row[u]);
                 xv[u] = __ldg((gen ? s.xbar : s.x) + row[u]);  // gen rows: the previous xbar
-                if (gen) gp[u] = load_gen_row(n, row[u]);
+                if (gen) gp[u] = load_gen_row(n, __ldg(n.rid + row[u]));
             }
         }
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u)
             if (row[u] >= 0 && kZY && (g[u] == 2 || g[u] == 3))
-                xv[u] = gen_row_x(row[u], gp[u], xv[u], zv[u], yv[u], q[u]);
+                xv[u] = gen_row_x(g[u] == 2 ? 0 : 1, gp[u], xv[u], zv[u], yv[u], q[u]);
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
             if (row[u] < 0) continue;
@@ -340,7 +339,7 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
                 s_a[p] = q[u];
                 s_b[p] = c;
             } else {
-                if (!sfinite(c)) atomicOr(&s_gl[slot[u]][7], kFlagNonfinite);
+                if (!sfinite(c)) atomicOr(&s_gl[slot[u]][3], kFlagNonfinite);
                 const double a = g[u] < 4 ? 1.0 : -1.0;  // gen columns +1, flow columns -1
                 s_a[p] = a * a / q[u];
                 s_b[p] = a * c / q[u];
@@ -349,19 +348,21 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
     }
     __syncthreads();
 
-    // 2. solve (thread = bus), kernels.cpp:303-391
+    // 2. solve (thread = bus), kernels.cpp:303-391; every group is a strided
+    // walk of the segment in the reference's push order
     if (i >= 0) {
         const int base = my_off;
-        const int* rows = n.bus_rows + s_base[tid];
-        const bool ref = (s_gl[tid][7] & kFlagRef) != 0;
+        const int start = s_base[tid];
+        const bool ref = (s_gl[tid][3] & kFlagRef) != 0;
         const int nc = ref ? 3 : 2;
         const double gs = n.b_gs[i], bs = n.b_bs[i];
         auto raw = [&](int k, double* q, double* c) {
-            const int row = rows[k];
+            const int row = start + k;
             *q = s.rho[row];
-            const double xr = (kZY && k >= gl[2] && k < gl[4])
-                                  ? gen_row_x(row, load_gen_row(n, row), s.xbar[row], s.z[row],
-                                              s.y[row], *q)
+            const int grp = group_of(ge, qs, k);
+            const double xr = (kZY && (grp == 2 || grp == 3))
+                                  ? gen_row_x(grp == 2 ? 0 : 1, load_gen_row(n, n.rid[row]),
+                                              s.xbar[row], s.z[row], s.y[row], *q)
                                   : s.x[row];
             *c = *q * (xr + s.z[row]) + s.y[row];
         };
@@ -371,15 +372,18 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
             else raw(k, q, c);
         };
         double q0 = 0.0, c0 = 0.0, q1 = 0.0, c1 = 0.0, q, c;
-        for (int k = 0; k < gl[1]; ++k) { staged_qc(k, &q, &c); q0 += q; c0 += c; }
-        for (int k = gl[1]; k < gl[2]; ++k) { staged_qc(k, &q, &c); q1 += q; c1 += c; }
+        for (int k = qs + 2; k < cnt; k += 4) { staged_qc(k, &q, &c); q0 += q; c0 += c; }
+        for (int k = qs + 3; k < cnt; k += 4) { staged_qc(k, &q, &c); q1 += q; c1 += c; }
         if (q0 == 0.0) q0 = 1.0;
         if (q1 == 0.0) q1 = 1.0;
-        bool finite = sfinite(c0) && sfinite(c1) && !(s_gl[tid][7] & kFlagNonfinite);
-        for (int k = max(gl[2], kStage - base); k < gl[6] && finite; ++k) {
+        bool finite = sfinite(c0) && sfinite(c1) && !(s_gl[tid][3] & kFlagNonfinite);
+        for (int k = (kStage - base > 0 ? kStage - base : 0); k < cnt && finite; ++k) {
+            const int grp = group_of(ge, qs, k);
+            if (grp < 2 || grp == 6) continue;
             raw(k, &q, &c);
             finite = sfinite(c);
         }
+        const int ngb = ge / 2, nq = (cnt - qs) / 4;
         double S[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, rhs[3] = {0, 0, 0};
         const double bvec[3] = {n.b_pd[i], n.b_qd[i], 0.0};
         if (finite) {
@@ -402,25 +406,30 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
                 *tr = a * c / q;
             };
             double ts, tr;
-            for (int k = gl[2]; k < gl[3]; ++k) { term(k, 1.0, &ts, &tr); s00 += ts; r0 += tr; }
-            for (int k = gl[4]; k < gl[5]; ++k) { term(k, -1.0, &ts, &tr); s00 += ts; r0 += tr; }
-            for (int k = gl[3]; k < gl[4]; ++k) { term(k, 1.0, &ts, &tr); s11 += ts; r1 += tr; }
-            for (int k = gl[5]; k < gl[6]; ++k) { term(k, -1.0, &ts, &tr); s11 += ts; r1 += tr; }
+            for (int k = 0; k < ge; k += 2) { term(k, 1.0, &ts, &tr); s00 += ts; r0 += tr; }
+            for (int k = qs; k < cnt; k += 4) { term(k, -1.0, &ts, &tr); s00 += ts; r0 += tr; }
+            for (int k = 1; k < ge; k += 2) { term(k, 1.0, &ts, &tr); s11 += ts; r1 += tr; }
+            for (int k = qs + 1; k < cnt; k += 4) { term(k, -1.0, &ts, &tr); s11 += ts; r1 += tr; }
             S[0] = s00; S[1] = s01; S[3] = s01; S[4] = s11;
             S[8] = s22;
             rhs[0] = r0 - bvec[0];
             rhs[1] = r1 - bvec[1];
             rhs[2] = r2 - bvec[2];
         } else {
-            // dense reference loop (kernels.cpp:350-361), any column value
+            // dense reference loop (kernels.cpp:350-361) over the columns
+            // [w, theta, gen_p..., gen_q..., flow_p..., flow_q...], any value
             auto col = [&](int j, int* gg, double* qj, double* cj) {
                 if (j == 0) { *gg = 0; *qj = q0; *cj = c0; return; }
                 if (j == 1) { *gg = 1; *qj = q1; *cj = c1; return; }
-                const int k = gl[2] + (j - 2);
-                *gg = group_of(gl, k);
+                const int d = j - 2;
+                int k;
+                if (d < ngb) { *gg = 2; k = 2 * d; }
+                else if (d < 2 * ngb) { *gg = 3; k = 2 * (d - ngb) + 1; }
+                else if (d < 2 * ngb + nq) { *gg = 4; k = qs + 4 * (d - 2 * ngb); }
+                else { *gg = 5; k = qs + 4 * (d - 2 * ngb - nq) + 1; }
                 raw(k, qj, cj);
             };
-            const int nv = 2 + (gl[6] - gl[2]);
+            const int nv = 2 + 2 * ngb + 2 * nq;
             for (int r = 0; r < nc; ++r) {
                 for (int t2 = 0; t2 < nc; ++t2) {
                     double acc = 0.0;
@@ -455,7 +464,7 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
             s_res[tid][4] = th;
         } else {
             atomicMin(&sc->singular_bus, i);
-            s_gl[tid][7] |= kFlagSingular;
+            s_gl[tid][3] |= kFlagSingular;
         }
         s_res[tid][0] = mu[0];
         s_res[tid][1] = mu[1];
@@ -475,7 +484,7 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
             if (p < total) {
                 int k;
                 locate(p, &slot[u], &k, &g[u]);
-                row[u] = __ldg(n.bus_rows + s_base[slot[u]] + k);
+                if (g[u] != 6) row[u] = s_base[slot[u]] + k;
             }
         }
         double old[kUnroll], q[kUnroll], xv[kUnroll], zv[kUnroll], yv[kUnroll], lam[kUnroll];
@@ -488,21 +497,21 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
                 zv[u] = __ldg(s.z + row[u]);
                 yv[u] = __ldg(s.y + row[u]);
                 xv[u] = __ldg(s.x + row[u]);  // generator rows: replaced below
-                if (kZY && (g[u] == 2 || g[u] == 3)) gp[u] = load_gen_row(n, row[u]);
+                if (kZY && (g[u] == 2 || g[u] == 3)) gp[u] = load_gen_row(n, __ldg(n.rid + row[u]));
                 if (kZY) lam[u] = __ldg(s.lambda + row[u]);
             }
         }
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
             if (row[u] >= 0 && kZY && (g[u] == 2 || g[u] == 3)) {
-                xv[u] = gen_row_x(row[u], gp[u], old[u], zv[u], yv[u], q[u]);
+                xv[u] = gen_row_x(g[u] == 2 ? 0 : 1, gp[u], old[u], zv[u], yv[u], q[u]);
                 s.x[row[u]] = xv[u];
             }
         }
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
             if (row[u] < 0) continue;
-            const int flags = s_gl[slot[u]][7];
+            const int flags = s_gl[slot[u]][3];
             double xb = old[u];
             if (!(flags & kFlagSingular)) {
                 if (g[u] == 0) xb = s_res[slot[u]][3];
@@ -567,7 +576,7 @@ __global__ void clamp_gen_p_kernel(DevNet n, DevState s) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n.gens_count()) return;
     const int g = n.gen_at(t);
-    const int pr = 2 * g;
+    const int pr = n.gpos[g];
     s.x[pr] = sclamp(s.x[pr], n.g_pmin[g], n.g_pmax[g]);
     s.xbar[pr] = sclamp(s.xbar[pr], n.g_pmin[g], n.g_pmax[g]);
 }

@@ -152,6 +152,11 @@ void Session::upload_network() {
         if (!host.empty())
             puts.push_back({reinterpret_cast<void**>(&dst), host.data(), host.size() * sizeof(host[0])});
     };
+    std::vector<std::vector<int>> keep;  // host copies that must outlive the uploads
+    auto put_copy = [&](int*& dst, std::vector<int>&& v) {
+        keep.push_back(std::move(v));
+        put(dst, keep.back());
+    };
     // generators
     std::vector<double> pmin(ng), pmax(ng), qmin(ng), qmax(ng), c2(ng), c1(ng);
     for (int g = 0; g < ng; ++g) {
@@ -201,13 +206,29 @@ void Session::upload_network() {
     alloc(dn_.b_vmin, nb); put(dn_.b_vmin, vmin);
     alloc(dn_.b_vmax, nb); put(dn_.b_vmax, vmax);
     trace_phase("upload: host SoA");
-    const BusCsr csr = build_bus_csr(net_);
-    trace_phase("upload: bus CSR");
-    alloc(dn_.bus_grp, csr.grp.size()); put(dn_.bus_grp, csr.grp);
-    alloc(dn_.bus_rows, csr.rows.size()); put(dn_.bus_rows, csr.rows);
+    layout_ = build_row_layout(net_);
+    trace_phase("upload: row layout");
+    const int mpad = layout_.mpad;
+    dn_.mpad = mpad;
+    {
+        std::vector<int> seg(4 * static_cast<size_t>(nb));
+        std::vector<int> ngen(nb, 0);
+        for (int g = 0; g < ng; ++g) ++ngen[net_.gens[g].bus];
+        for (int i = 0; i < nb; ++i) {
+            seg[4 * i] = layout_.seg[3 * i];
+            seg[4 * i + 1] = layout_.seg[3 * i] + 2 * ngen[i];
+            seg[4 * i + 2] = layout_.seg[3 * i + 1];
+            seg[4 * i + 3] = layout_.seg[3 * i + 2];
+        }
+        alloc(dn_.bus_seg, seg.size()); put_copy(dn_.bus_seg, std::move(seg));
+    }
+    alloc(dn_.gpos, layout_.gpos.size()); put(dn_.gpos, layout_.gpos);
+    alloc(dn_.qpos, layout_.qpos.size()); put(dn_.qpos, layout_.qpos);
+    alloc(dn_.quad_branch, layout_.quad_branch.size()); put(dn_.quad_branch, layout_.quad_branch);
+    alloc(dn_.rid, layout_.rid.size()); put(dn_.rid, layout_.rid);
     // state
-    alloc(ds_.x, m); alloc(ds_.xbar, m); alloc(ds_.z, m); alloc(ds_.y, m);
-    alloc(ds_.lambda, m); alloc(ds_.rho, m);
+    alloc(ds_.x, mpad); alloc(ds_.xbar, mpad); alloc(ds_.z, mpad); alloc(ds_.y, mpad);
+    alloc(ds_.lambda, mpad); alloc(ds_.rho, mpad);
     alloc(ds_.bus_w, nb); alloc(ds_.bus_theta, nb);
     alloc(ds_.bp, 6 * static_cast<size_t>(nl));
     alloc(ds_.lt_ij, nl); alloc(ds_.lt_ji, nl); alloc(ds_.rho_t, nl);
@@ -223,15 +244,21 @@ void Session::upload_network() {
     if (plan_.parts > 1) {
         alloc(dn_.own_gens, plan_.gens.size()); put(dn_.own_gens, plan_.gens);
         alloc(dn_.own_buses, plan_.buses.size()); put(dn_.own_buses, plan_.buses);
-        alloc(dn_.own_rows, plan_.rows.size()); put(dn_.own_rows, plan_.rows);
+        // plan rows are reference row ids; the device works on positions
+        auto to_pos = [&](const std::vector<int>& rows) {
+            std::vector<int> p(rows.size());
+            for (size_t k = 0; k < rows.size(); ++k) p[k] = layout_.pos[rows[k]];
+            return p;
+        };
+        alloc(dn_.own_rows, plan_.rows.size()); put_copy(dn_.own_rows, to_pos(plan_.rows));
         dn_.n_own_gens = static_cast<int>(plan_.gens.size());
         dn_.n_own_buses = static_cast<int>(plan_.buses.size());
         dn_.n_own_rows = static_cast<int>(plan_.rows.size());
         d_send_.assign(plan_.parts, nullptr);
         d_recv_.assign(plan_.parts, nullptr);
         for (int q = 0; q < plan_.parts; ++q) {
-            alloc(d_send_[q], plan_.send_x[q].size()); put(d_send_[q], plan_.send_x[q]);
-            alloc(d_recv_[q], plan_.recv_x[q].size()); put(d_recv_[q], plan_.recv_x[q]);
+            alloc(d_send_[q], plan_.send_x[q].size()); put_copy(d_send_[q], to_pos(plan_.send_x[q]));
+            alloc(d_recv_[q], plan_.recv_x[q].size()); put_copy(d_recv_[q], to_pos(plan_.recv_x[q]));
         }
     }
     if (plan_.parts <= 1) {
@@ -239,6 +266,7 @@ void Session::upload_network() {
         alloc(ext_.vm, nb);
         alloc(ext_.va, nb);
         alloc(ext_.cand, nl);
+        alloc(ext_.gen_pq, 2 * static_cast<size_t>(ng));
         alloc(ext_.sc, 1);
     }
     alloc(sc_, 1);
@@ -282,8 +310,19 @@ void Session::upload_state(const HostState& s) {
                                   stream_),
                   "upload_state");
     };
-    put(ds_.x, s.x); put(ds_.xbar, s.xbar); put(ds_.z, s.z); put(ds_.y, s.y);
-    put(ds_.lambda, s.lambda); put(ds_.rho, s.rho);
+    // row vectors: reference row order (host) -> storage positions (device)
+    std::vector<std::vector<double>> rowbuf;
+    auto put_rows = [&](double* dst, const std::vector<double>& v) {
+        if (v.empty()) return;
+        if (v.size() != layout_.pos.size()) throw std::invalid_argument("state row vector size");
+        rowbuf.emplace_back(static_cast<size_t>(dn_.mpad), 0.0);
+        std::vector<double>& p = rowbuf.back();
+        for (size_t r = 0; r < v.size(); ++r) p[layout_.pos[r]] = v[r];
+        put(dst, p);
+    };
+    rowbuf.reserve(6);
+    put_rows(ds_.x, s.x); put_rows(ds_.xbar, s.xbar); put_rows(ds_.z, s.z); put_rows(ds_.y, s.y);
+    put_rows(ds_.lambda, s.lambda); put_rows(ds_.rho, s.rho);
     put(ds_.bus_w, s.bus_w); put(ds_.bus_theta, s.bus_theta);
     if (!s.bp.empty()) {  // branch-major (host) -> component-major (device)
         std::vector<double> t(6 * nl);
@@ -308,13 +347,19 @@ void Session::download_state(HostState& s) const {
         if (n) check(cudaMemcpyAsync(v.data(), src, n * sizeof(double), cudaMemcpyDeviceToHost, stream_),
                      "download_state");
     };
-    get(s.x, ds_.x, m); get(s.xbar, ds_.xbar, m); get(s.z, ds_.z, m); get(s.y, ds_.y, m);
-    get(s.lambda, ds_.lambda, m); get(s.rho, ds_.rho, m);
+    std::vector<double> rows[6];
+    const double* srcs[6] = {ds_.x, ds_.xbar, ds_.z, ds_.y, ds_.lambda, ds_.rho};
+    for (int k = 0; k < 6; ++k) get(rows[k], srcs[k], static_cast<size_t>(dn_.mpad));
     get(s.bus_w, ds_.bus_w, nb); get(s.bus_theta, ds_.bus_theta, nb);
     std::vector<double> t;
     get(t, ds_.bp, 6 * nl);
     get(s.lt_ij, ds_.lt_ij, nl); get(s.lt_ji, ds_.lt_ji, nl); get(s.rho_t, ds_.rho_t, nl);
     check(cudaStreamSynchronize(stream_), "sync");
+    std::vector<double>* dst[6] = {&s.x, &s.xbar, &s.z, &s.y, &s.lambda, &s.rho};
+    for (int k = 0; k < 6; ++k) {  // storage positions -> reference row order
+        dst[k]->resize(m);
+        for (int r = 0; r < m; ++r) (*dst[k])[r] = rows[k][layout_.pos[r]];
+    }
     s.bp.resize(6 * nl);
     for (size_t b = 0; b < nl; ++b)
         for (int k = 0; k < 6; ++k) s.bp[6 * b + k] = t[k * nl + b];
@@ -327,8 +372,9 @@ void Session::download_solution_inputs(std::vector<double>& gen_rows, std::vecto
     gen_rows.resize(2 * static_cast<size_t>(dn_.ng));
     w.resize(dn_.nb);
     th.resize(dn_.nb);
-    if (!gen_rows.empty())
-        check(cudaMemcpyAsync(gen_rows.data(), ds_.x, gen_rows.size() * sizeof(double),
+    std::vector<double> xall(static_cast<size_t>(dn_.mpad));
+    if (!xall.empty())
+        check(cudaMemcpyAsync(xall.data(), ds_.x, xall.size() * sizeof(double),
                               cudaMemcpyDeviceToHost, stream_), "D2H");
     if (dn_.nb) {
         check(cudaMemcpyAsync(w.data(), ds_.bus_w, w.size() * sizeof(double), cudaMemcpyDeviceToHost,
@@ -337,6 +383,10 @@ void Session::download_solution_inputs(std::vector<double>& gen_rows, std::vecto
                               cudaMemcpyDeviceToHost, stream_), "D2H");
     }
     check(cudaStreamSynchronize(stream_), "sync");
+    for (int g = 0; g < dn_.ng; ++g) {  // generator rows in reference order
+        gen_rows[2 * static_cast<size_t>(g)] = xall[layout_.gpos[g]];
+        gen_rows[2 * static_cast<size_t>(g) + 1] = xall[layout_.gpos[g] + 1];
+    }
 }
 
 BranchCfg branch_cfg(const SolverConfig& c);
@@ -440,7 +490,7 @@ bool Session::extract_on_device(Solution& sol, QualityMetrics& q) {
     auto d2h = [&](void* dst, const void* src, size_t bytes) {
         if (bytes) check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream_), "D2H");
     };
-    d2h(gen_rows.data(), ds_.x, gen_rows.size() * sizeof(double));
+    d2h(gen_rows.data(), ext_.gen_pq, gen_rows.size() * sizeof(double));
     d2h(sol.vm.data(), ext_.vm, nb * sizeof(double));
     d2h(sol.va.data(), ext_.va, nb * sizeof(double));
     d2h(sol.flows.data(), ext_.flows, sol.flows.size() * sizeof(double));
@@ -674,7 +724,7 @@ void Session::outer_update() {
 
 double Session::rho_max() {
     use_device();
-    launch_rowmax(ds_.rho, dn_.m, red_, stream_);
+    launch_rowmax(ds_.rho, dn_.mpad, red_, stream_);
     unsigned long long bits = 0;
     check(cudaMemcpyAsync(&bits, red_, sizeof bits, cudaMemcpyDeviceToHost, stream_), "D2H");
     check(cudaStreamSynchronize(stream_), "sync");

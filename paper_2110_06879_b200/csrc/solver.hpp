@@ -232,6 +232,7 @@ private:
     DevNet dn_;
     DevState ds_;
     DevExtract ext_;  // single-part sessions only
+    RowLayout layout_;  // device storage order of the rows
     // graph path (inner_loop): control block, records, the captured batch
     LoopCtl* ctl_ = nullptr;
     LoopCtl* ctl_host_ = nullptr;  // pinned

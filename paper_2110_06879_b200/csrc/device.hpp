@@ -31,6 +31,10 @@ struct DevNet {
     // generators
     double *g_pmin = nullptr, *g_pmax = nullptr, *g_qmin = nullptr, *g_qmax = nullptr;
     double *g_c2 = nullptr, *g_c1 = nullptr;
+    // the same generator data in storage order, indexed by position / 2 of
+    // the generator's (p, q) pair (read by the bus kernel without indirection)
+    double *pr_c1 = nullptr, *pr_c2 = nullptr, *pr_pmin = nullptr, *pr_pmax = nullptr;
+    double *pr_qmin = nullptr, *pr_qmax = nullptr;
     // branches
     int *br_from = nullptr, *br_to = nullptr;
     double* br_y = nullptr;     // [8][nl]: gii bii gij bij gji bji gjj bjj

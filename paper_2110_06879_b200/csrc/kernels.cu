@@ -77,18 +77,19 @@ __global__ void __launch_bounds__(kBlock) gen_kernel(DevNet n, DevState s) {
 struct GenRow {
     double c1, c2, lo, hi;  // p row: c1, c2, pmin, pmax; q row: -, -, qmin, qmax
 };
-__device__ __forceinline__ GenRow load_gen_row(const DevNet& n, int row) {
-    const int g = row >> 1;
+// pos: the storage position of a generator row (p rows at even positions)
+__device__ __forceinline__ GenRow load_gen_row(const DevNet& n, int pos) {
+    const int h = pos >> 1;
     GenRow r;
-    if ((row & 1) == 0) {
-        r.c1 = __ldg(n.g_c1 + g);
-        r.c2 = __ldg(n.g_c2 + g);
-        r.lo = __ldg(n.g_pmin + g);
-        r.hi = __ldg(n.g_pmax + g);
+    if ((pos & 1) == 0) {
+        r.c1 = __ldg(n.pr_c1 + h);
+        r.c2 = __ldg(n.pr_c2 + h);
+        r.lo = __ldg(n.pr_pmin + h);
+        r.hi = __ldg(n.pr_pmax + h);
     } else {
         r.c1 = r.c2 = 0.0;
-        r.lo = __ldg(n.g_qmin + g);
-        r.hi = __ldg(n.g_qmax + g);
+        r.lo = __ldg(n.pr_qmin + h);
+        r.hi = __ldg(n.pr_qmax + h);
     }
     return r;
 }
@@ -323,7 +324,7 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
                 zv[u] = __ldg(s.z + row[u]);
                 yv[u] = __ldg(s.y + row[u]);
                 xv[u] = __ldg((gen ? s.xbar : s.x) + row[u]);  // gen rows: the previous xbar
-                if (gen) gp[u] = load_gen_row(n, __ldg(n.rid + row[u]));
+                if (gen) gp[u] = load_gen_row(n, row[u]);
             }
         }
 #pragma unroll
@@ -361,7 +362,7 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
             *q = s.rho[row];
             const int grp = group_of(ge, qs, k);
             const double xr = (kZY && (grp == 2 || grp == 3))
-                                  ? gen_row_x(grp == 2 ? 0 : 1, load_gen_row(n, n.rid[row]),
+                                  ? gen_row_x(grp == 2 ? 0 : 1, load_gen_row(n, row),
                                               s.xbar[row], s.z[row], s.y[row], *q)
                                   : s.x[row];
             *c = *q * (xr + s.z[row]) + s.y[row];
@@ -497,7 +498,7 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
                 zv[u] = __ldg(s.z + row[u]);
                 yv[u] = __ldg(s.y + row[u]);
                 xv[u] = __ldg(s.x + row[u]);  // generator rows: replaced below
-                if (kZY && (g[u] == 2 || g[u] == 3)) gp[u] = load_gen_row(n, __ldg(n.rid + row[u]));
+                if (kZY && (g[u] == 2 || g[u] == 3)) gp[u] = load_gen_row(n, row[u]);
                 if (kZY) lam[u] = __ldg(s.lambda + row[u]);
             }
         }

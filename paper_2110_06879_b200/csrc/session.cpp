@@ -1,6 +1,7 @@
 // session.cpp — device residency of one network + AdmmState and the phase
 // sequence of one inner iteration (proj/src/driver.cpp:155-186).
 #include <algorithm>
+#include <deque>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -153,6 +154,7 @@ void Session::upload_network() {
             puts.push_back({reinterpret_cast<void**>(&dst), host.data(), host.size() * sizeof(host[0])});
     };
     std::vector<std::vector<int>> keep;  // host copies that must outlive the uploads
+    std::deque<std::vector<double>> keepd;
     auto put_copy = [&](int*& dst, std::vector<int>&& v) {
         keep.push_back(std::move(v));
         put(dst, keep.back());
@@ -223,6 +225,25 @@ void Session::upload_network() {
         alloc(dn_.bus_seg, seg.size()); put_copy(dn_.bus_seg, std::move(seg));
     }
     alloc(dn_.gpos, layout_.gpos.size()); put(dn_.gpos, layout_.gpos);
+    {
+        const size_t np = static_cast<size_t>(mpad) / 2 + 1;
+        std::vector<double>* pr[6];
+        for (auto& p : pr) {
+            keepd.emplace_back(np, 0.0);
+            p = &keepd.back();
+        }
+        for (int g = 0; g < ng; ++g) {
+            const size_t h = static_cast<size_t>(layout_.gpos[g]) / 2;
+            (*pr[0])[h] = c1[g]; (*pr[1])[h] = c2[g]; (*pr[2])[h] = pmin[g];
+            (*pr[3])[h] = pmax[g]; (*pr[4])[h] = qmin[g]; (*pr[5])[h] = qmax[g];
+        }
+        double** dst[6] = {&dn_.pr_c1, &dn_.pr_c2, &dn_.pr_pmin, &dn_.pr_pmax, &dn_.pr_qmin,
+                           &dn_.pr_qmax};
+        for (int k = 0; k < 6; ++k) {
+            alloc(*dst[k], np);
+            put(*dst[k], *pr[k]);
+        }
+    }
     alloc(dn_.qpos, layout_.qpos.size()); put(dn_.qpos, layout_.qpos);
     alloc(dn_.quad_branch, layout_.quad_branch.size()); put(dn_.quad_branch, layout_.quad_branch);
     alloc(dn_.rid, layout_.rid.size()); put(dn_.rid, layout_.rid);
@@ -530,6 +551,20 @@ void Session::set_gen_p_bounds(const std::vector<double>& pmin, const std::vecto
                           cudaMemcpyHostToDevice, stream_), "set_gen_p_bounds");
     check(cudaMemcpyAsync(dn_.g_pmax, pmax.data(), pmax.size() * sizeof(double),
                           cudaMemcpyHostToDevice, stream_), "set_gen_p_bounds");
+    {  // and the storage-order copy the bus kernel reads
+        const size_t np = static_cast<size_t>(dn_.mpad) / 2 + 1;
+        std::vector<double> lo(np, 0.0), hi(np, 0.0);
+        for (size_t g = 0; g < pmin.size(); ++g) {
+            const size_t h = static_cast<size_t>(layout_.gpos[g]) / 2;
+            lo[h] = pmin[g];
+            hi[h] = pmax[g];
+        }
+        check(cudaMemcpyAsync(dn_.pr_pmin, lo.data(), np * sizeof(double), cudaMemcpyHostToDevice,
+                              stream_), "set_gen_p_bounds");
+        check(cudaMemcpyAsync(dn_.pr_pmax, hi.data(), np * sizeof(double), cudaMemcpyHostToDevice,
+                              stream_), "set_gen_p_bounds");
+        check(cudaStreamSynchronize(stream_), "sync");
+    }
     check(cudaStreamSynchronize(stream_), "sync");
     for (size_t g = 0; g < pmin.size() && g < net_.gens.size(); ++g) {  // ramp window
         net_.gens[g].pmin = pmin[g];

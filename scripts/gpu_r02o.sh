@@ -1,0 +1,8 @@
+#!/bin/bash
+O=gpurun_out/o
+mkdir -p $O
+for v in bb64 bb32 default; do
+  L=paper_2110_06879_b200/libgridadmm_$v.so; [ $v = default ] && L=paper_2110_06879_b200/libgridadmm.so
+  GRIDADMM_LIB=$L timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-converge --no-track > $O/bench_$v.json 2>&1
+done
+echo done

@@ -159,11 +159,12 @@ gridadmm_status gridadmm_session_kernel_time(const gridadmm_session* s,
                                              int kernel_class, double* ms,
                                              long long* launches);
 
-/* Cumulative TRON iterations executed by the branch kernel (lean flop
- * census input) and branch-kernel launches. */
+/* Cumulative TRON iterations of all branch solves since the session began
+ * (the reference's count, tron.hpp:34-39) and the part of them spent on the
+ * rate-limited (6-variable) branches. */
 gridadmm_status gridadmm_session_counters(const gridadmm_session* s,
                                           long long* tron_iterations,
-                                          long long* sincos_calls);
+                                          long long* limited_iterations);
 
 /* Cumulative counters: out[0], out[1] = TRON iterations with the reference's
  * accounting (TronResult::iterations; 4-var, 6-var branches), out[2],

@@ -461,6 +461,7 @@ class Session:
         return tuple(out)
 
     def counters(self):
+        """(TRON iterations of all branch solves, of the rate-limited ones)."""
         t = ctypes.c_longlong()
         s = ctypes.c_longlong()
         _check(lib().gridadmm_session_counters(self._h, ctypes.byref(t), ctypes.byref(s)))

@@ -547,11 +547,11 @@ gridadmm_status gridadmm_session_kernel_time(const gridadmm_session* s, int cls,
 }
 
 gridadmm_status gridadmm_session_counters(const gridadmm_session* s, long long* tron_iterations,
-                                          long long* sincos_calls) {
+                                          long long* limited_iterations) {
     if (!s || !s->s) return fail(GRIDADMM_ERR_INVALID_ARG, "counters need a single-part session");
     return guarded([&]() -> gridadmm_status {
         if (tron_iterations) *tron_iterations = s->s->tron_iterations();
-        if (sincos_calls) *sincos_calls = s->s->sincos_calls();
+        if (limited_iterations) *limited_iterations = s->s->limited_tron_iterations();
         return GRIDADMM_OK;
     });
 }

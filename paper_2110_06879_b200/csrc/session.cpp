@@ -773,7 +773,7 @@ long long Session::tron_iterations() const {
     return static_cast<long long>(h.tron_iters4);
 }
 
-long long Session::sincos_calls() const {
+long long Session::limited_tron_iterations() const {
     use_device();
     DevScalars h;
     check(cudaMemcpy(&h, sc_, sizeof h, cudaMemcpyDeviceToHost), "D2H");

@@ -213,7 +213,7 @@ public:
     void branch_costs(int* out) const;
     // TRON iterations (reference semantics) and executed steps, 4-/6-var.
     void step_counters(long long out[4]) const;
-    long long sincos_calls() const;
+    long long limited_tron_iterations() const;  // 6-variable branches only
     void sync() const;
 
     bool extract_on_device(Solution& sol, QualityMetrics& q) override;

@@ -132,3 +132,20 @@ def test_partitioned_synthetic_grid(gridadmm):
     r1, _ = s1.iterate(25)
     r4, _ = s4.iterate(25)
     assert np.array_equal(r1.view(np.uint64), r4.view(np.uint64))
+
+
+@pytest.mark.gpu
+def test_nccl_engine_single_rank_bit_identical(gridadmm):
+    """The one-process-per-GPU engine (dist.cpp: NCCL loaded with dlopen, the
+    norms all-reduced, the exchange plan of a 1-part partition) on this box's
+    single GPU: same residual series and state as the plain session."""
+    net = gridadmm.Network(case_path("case118"))
+    cfg = gridadmm.Config("case118", eps=1e-5)
+    s1 = gridadmm.Session(net, cfg)
+    sd = gridadmm.Session.distributed(net, cfg, 0, 1, gridadmm.nccl_unique_id())
+    r1, _ = s1.iterate(60)
+    rd, _ = sd.iterate(60)
+    assert np.array_equal(r1.view(np.uint64), rd.view(np.uint64))
+    a, b = s1.get_state(), sd.get_state()
+    for f in a:
+        assert np.array_equal(a[f].view(np.uint64), b[f].view(np.uint64)), f

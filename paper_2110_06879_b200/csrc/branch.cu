@@ -454,13 +454,13 @@ __global__ void __launch_bounds__(kTileBlock, GA_TILE_MINB) tile_kernel(DevNet n
     int fails = 0;
     // Tail mode: when a queue holds no more branches than half the grid's
     // warps, each branch gets a whole warp (T = 32: no other tile diverging in
-    // its warp, 32 search trials per round); otherwise 8-lane tiles.
+    // its warp, 32 search trials per round); otherwise kTile-lane tiles.
 #ifndef GA_TILE_TAIL
 #define GA_TILE_TAIL 1
 #endif
     const int half_warps =
         GA_TILE_TAIL ? (int)(gridDim.x * (kTileBlock / 32) * cfg.tail_num / 4) : -1;
-    // 8-lane tiles hand branches that exceed cfg.tile_budget steps to the
+    // kTile-lane tiles hand branches that exceed cfg.tile_budget steps to the
     // solo phase (one warp per branch, one block per SM).
     auto run6 = [&] {
         if (w.ctr[2] <= half_warps)

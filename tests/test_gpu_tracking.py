@@ -55,3 +55,30 @@ def test_tracking_per_bus_profile_and_ramp(gridadmm, oracle_mod, tmp_path):
         m = trk.period_report(p).metrics()
         assert m["inner_iterations"] == rm["inner_iterations"]
         assert bits(m["objective"]) == bits(rm["objective"])
+
+
+def test_empty_ramp_window_is_infeasible_ramp(gridadmm, oracle_mod, tmp_path):
+    """RampError -> GRIDADMM_ERR_INFEASIBLE_RAMP (tracking.cpp:48-60,
+    capi.cpp:302-303): a generator with pmax < 0 has ramp window
+    [prev + |r|, prev - |r|] in period 2, empty for any prev_pg.  Same status,
+    same message, no tracking handle."""
+    import ctypes
+    src = open(case_path("case9")).read()
+    row = "\t3\t85\t-10.95\t300\t-300\t1.025\t100\t1\t270\t10\t"
+    assert row in src
+    case = tmp_path / "case9_negpmax.m"
+    case.write_text(src.replace(row, "\t3\t-15\t-10.95\t300\t-300\t1.025\t100\t1\t-10\t-20\t"))
+    csv = tmp_path / "profile.csv"
+    csv.write_text("period,multiplier\n1,1.0\n2,1.01\n")
+    extra = dict(eps=1e-4, max_outer=2, max_inner=40)
+    net = gridadmm.Network(str(case))
+    cfg = gridadmm.Config("case9", **extra)
+    h = ctypes.c_void_p()
+    st = gridadmm.lib().gridadmm_track_run(net.handle, cfg.handle, str(csv).encode(), ctypes.byref(h))
+    msg = gridadmm.lib().gridadmm_last_error().decode()
+    ref_st, ref = oracle_mod.ref_track(str(case), str(csv), "case9", **extra)
+    ref_msg = oracle_mod.ref_capi().gridadmm_last_error().decode()
+    assert st == ref_st == 6, (st, ref_st, msg, ref_msg)  # GRIDADMM_ERR_INFEASIBLE_RAMP
+    assert not h.value and ref == []
+    assert msg == ref_msg, (msg, ref_msg)
+    assert "empty ramp window for generator 2 in period 2" in msg

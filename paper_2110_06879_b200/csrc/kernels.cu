@@ -195,7 +195,13 @@ __device__ __forceinline__ bool ge_solve(double* S, double* rhs, double* mu) {
 #ifndef GA_BUS_BLOCK
 #define GA_BUS_BLOCK 128
 #endif
-constexpr int kBB = GA_BUS_BLOCK;  // buses (threads) per block
+constexpr int kBB = GA_BUS_BLOCK;  // buses per block
+// Threads per block kBT = kTPB * kBB: the per-row phases (gather, write) use
+// all of them, the per-bus solve the first kBB.  A block's time is its
+// per-thread row work plus the solve, so two threads per bus cut it by ~30%
+// (2868-shaped grid: 37.5 -> 26.7 us) — worth it while the grid fits in one
+// wave; on the 70k shape (547 blocks) the halved residency costs more
+// (73 -> 78 us), so launch_bus_* pick kTPB by grid size.
 // staged rows per block (the rest are read from global); 8 / 12 rows per bus
 // with 6-8 blocks per SM forced by __launch_bounds__ measured 23-43% slower
 constexpr int kStage = 16 * kBB;
@@ -229,8 +235,8 @@ __device__ __forceinline__ unsigned long long global_ns() {
     return t;
 }
 
-template <bool kZY>
-__global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, double beta,
+template <bool kZY, int kTPB>
+__global__ void __launch_bounds__(kTPB * kBB) bus_block_kernel(DevNet n, DevState s, double beta,
                                                        DevScalars* sc, LoopCtl* gate) {
     if (gate) {
         if (*reinterpret_cast<volatile int*>(&gate->stop)) return;
@@ -243,14 +249,15 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
     __shared__ double s_res[kBB][5];  // mu0..2, w, theta
     __shared__ double s_a[kStage], s_b[kStage];
     __shared__ unsigned short s_pos[kStage];  // staged position -> slot << 3 | group
-    __shared__ int s_wsum[kBB / 32];
+    constexpr int kBT = kTPB * kBB;
+    __shared__ int s_wsum[kBT / 32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int t = blockIdx.x * kBB + tid;
     const int nbus = n.buses_count();
     int i = -1, cnt = 0, ge = 0, qs = 0;
     {
         int start = 0;
-        if (t < nbus) {
+        if (tid < kBB && t < nbus) {
             i = n.bus_at(t);
             const int* seg = n.bus_seg + 4 * i;
             start = __ldg(seg);
@@ -258,11 +265,13 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
             qs = __ldg(seg + 2) - start;
             cnt = __ldg(seg + 3) - start;
         }
-        s_base[tid] = start;
-        s_gl[tid][0] = ge;
-        s_gl[tid][1] = qs;
-        s_gl[tid][2] = cnt;
-        s_gl[tid][3] = (i >= 0 && i == n.ref_bus) ? kFlagRef : 0;
+        if (tid < kBB) {
+            s_base[tid] = start;
+            s_gl[tid][0] = ge;
+            s_gl[tid][1] = qs;
+            s_gl[tid][2] = cnt;
+            s_gl[tid][3] = (i >= 0 && i == n.ref_bus) ? kFlagRef : 0;
+        }
     }
     // block exclusive scan of the segment lengths
     int incl = cnt;
@@ -277,7 +286,7 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
 #pragma unroll
     for (int w = 0; w < kBB / 32; ++w) woff += w < wid ? s_wsum[w] : 0;
     const int my_off = woff + incl - cnt;
-    s_off[tid] = my_off;
+    if (tid < kBB) s_off[tid] = my_off;
     if (tid == kBB - 1) s_off[kBB] = woff + incl;
     for (int k = 0; k < cnt && my_off + k < kStage; ++k)  // position map of the staged rows
         s_pos[my_off + k] = static_cast<unsigned short>(tid << 3 | group_of(ge, qs, k));
@@ -302,11 +311,11 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
     // (for one block of consecutive buses the positions are one contiguous
     // range of the row vectors: coalesced)
     constexpr int kUnroll = 4;
-    for (int p0 = tid; p0 < staged; p0 += kBB * kUnroll) {
+    for (int p0 = tid; p0 < staged; p0 += kBT * kUnroll) {
         int row[kUnroll], slot[kUnroll], g[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
-            const int p = p0 + u * kBB;
+            const int p = p0 + u * kBT;
             row[u] = -1;
             if (p < staged) {
                 int k;
@@ -334,7 +343,7 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
             if (row[u] < 0) continue;
-            const int p = p0 + u * kBB;
+            const int p = p0 + u * kBT;
             const double c = q[u] * (xv[u] + zv[u]) + yv[u];
             if (g[u] < 2) {
                 s_a[p] = q[u];
@@ -476,11 +485,11 @@ __global__ void __launch_bounds__(kBB) bus_block_kernel(DevNet n, DevState s, do
     // 3. write xbar (+ z, y) and the norms; the old values read here were
     // not written before in this kernel (each row belongs to one block)
     double dual = 0.0, pr = 0.0, zi = 0.0, zd = 0.0;
-    for (int p0 = tid; p0 < total; p0 += kBB * kUnroll) {
+    for (int p0 = tid; p0 < total; p0 += kBT * kUnroll) {
         int row[kUnroll], slot[kUnroll], g[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
-            const int p = p0 + u * kBB;
+            const int p = p0 + u * kBT;
             row[u] = -1;
             if (p < total) {
                 int k;
@@ -729,15 +738,38 @@ void launch_generators(const DevNet& n, const DevState& s, cudaStream_t st) {
     if (c > 0) gen_kernel<<<blocks_for(c), kBlock, 0, st>>>(n, s);
 }
 
+namespace {
+// two threads per bus while the grid fits in one wave at two blocks per SM
+bool bus_two_threads(int blocks) {
+    static const int sms = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return blocks <= 2 * sms;
+}
+}  // namespace
+
 void launch_buses(const DevNet& n, const DevState& s, DevScalars* sc, cudaStream_t st) {
     const int c = n.buses_count();
-    if (c > 0) bus_block_kernel<false><<<(c + kBB - 1) / kBB, kBB, 0, st>>>(n, s, 0.0, sc, nullptr);
+    if (c <= 0) return;
+    const int blocks = (c + kBB - 1) / kBB;
+    if (bus_two_threads(blocks))
+        bus_block_kernel<false, 2><<<blocks, 2 * kBB, 0, st>>>(n, s, 0.0, sc, nullptr);
+    else
+        bus_block_kernel<false, 1><<<blocks, kBB, 0, st>>>(n, s, 0.0, sc, nullptr);
 }
 
 void launch_bus_zy(const DevNet& n, const DevState& s, double beta, DevScalars* sc,
                    cudaStream_t st, LoopCtl* gate) {
     const int c = n.buses_count();
-    if (c > 0) bus_block_kernel<true><<<(c + kBB - 1) / kBB, kBB, 0, st>>>(n, s, beta, sc, gate);
+    if (c <= 0) return;
+    const int blocks = (c + kBB - 1) / kBB;
+    if (bus_two_threads(blocks))
+        bus_block_kernel<true, 2><<<blocks, 2 * kBB, 0, st>>>(n, s, beta, sc, gate);
+    else
+        bus_block_kernel<true, 1><<<blocks, kBB, 0, st>>>(n, s, beta, sc, gate);
 }
 
 void launch_z_only(const DevNet& n, const DevState& s, double beta, cudaStream_t st) {

@@ -12,16 +12,24 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 
 shape, preset = sys.argv[1], sys.argv[2]
+
+
+def config(**kw):
+    if ":" in preset:  # explicit "rho_pq:rho_va"
+        rpq, rva = (float(v) for v in preset.split(":"))
+        return ga.Config(rho_pq=rpq, rho_va=rva, **kw)
+    return ga.Config(preset, **kw)
+
 prof = os.path.join(tempfile.mkdtemp(), "prof.csv")
 os.environ["GRIDADMM_PROFILE"] = prof
 import paper_2110_06879_b200 as ga  # noqa: E402
 from gridcases import synth  # noqa: E402
 
 net = ga.Network(synth.ensure_case(shape, "/tmp/gridadmm_cases"))
-ga.solve(net, ga.Config(preset, max_outer=1, max_inner=2))
+ga.solve(net, config(max_outer=1, max_inner=2))
 open(prof, "w").close()
 t0 = time.perf_counter()
-st, rep = ga.solve(net, ga.Config(preset))
+st, rep = ga.solve(net, config())
 wall = time.perf_counter() - t0
 rows = np.genfromtxt(prof, delimiter=",", names=True)
 m = rep.metrics()

@@ -12,13 +12,22 @@ import paper_2110_06879_b200 as ga  # noqa: E402
 from gridcases import synth  # noqa: E402
 
 shape, preset, combos = sys.argv[1], sys.argv[2], json.loads(sys.argv[3])
+
+
+def config(**kw):
+    if ":" in preset:  # explicit "rho_pq:rho_va"
+        rpq, rva = (float(v) for v in preset.split(":"))
+        return ga.Config(rho_pq=rpq, rho_va=rva, **kw)
+    return ga.Config(preset, **kw)
+
+
 net = ga.Network(synth.ensure_case(shape, "/tmp/gridadmm_cases"))
-ga.solve(net, ga.Config(preset, max_outer=1, max_inner=3))
+ga.solve(net, config(max_outer=1, max_inner=3))
 for kw in combos:
     times = []
     for _ in range(2):
         t0 = time.perf_counter()
-        st, rep = ga.solve(net, ga.Config(preset, **kw))
+        st, rep = ga.solve(net, config(**kw))
         times.append(time.perf_counter() - t0)
     m = rep.metrics()
     print(json.dumps({"cfg": kw, "best_s": min(times), "inner": m["inner_iterations"],

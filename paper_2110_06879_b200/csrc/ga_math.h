@@ -29,6 +29,34 @@ GA_FN bool sfinite(double v) { return v - v == 0.0; }
 // running non-negative max (proj/src/decomp.cpp:67, driver.cpp:117-120,179-186).
 GA_FN double abs_or_zero(double v) { return (v == v) ? fabs(v) : 0.0; }
 
+// Largest double t with fl(sqrt(t)) <= d, so that for every double y
+//   (sqrt(y) <= d)  ==  (y <= t)
+// (sqrt is correctly rounded and monotone; NaN y fails both sides).  The
+// trust-region test ||s|| <= delta of the Cauchy search (tron.cpp:111,130)
+// then costs one compare per trial instead of a square root.  Valid for
+// d in [2^-400, 2^400]: fl(d*d) is normal there and fl(sqrt(fl(d*d))) == d
+// (round-to-nearest), and at most two successors of fl(d*d) still round to
+// d; *ok is false outside that range (the caller keeps the square root).
+// tests/c/sqrt_bound_check.cpp checks maximality and the equivalence.
+GA_FN double sqrt_le_bound(double d, bool* ok) {
+    *ok = d >= 0x1p-400 && d <= 0x1p400;
+    if (!*ok) return 0.0;
+    double t = d * d;
+#if defined(__CUDACC__)
+#pragma unroll 1
+#endif
+    for (int k = 0; k < 4; ++k) {  // one square-root site (code size)
+        long long bits;
+        __builtin_memcpy(&bits, &t, sizeof t);
+        ++bits;
+        double n;
+        __builtin_memcpy(&n, &bits, sizeof n);
+        if (!(sqrt(n) <= d)) break;
+        t = n;
+    }
+    return t;
+}
+
 }  // namespace ga
 
 #endif

@@ -122,8 +122,9 @@ GA_FN double vnorm2(const double* a) { return tsqrt<kOol>(vdot<N>(a, a)); }
 
 // q(s) = g's + sum_i 0.5*s_i*(H s)_i  (tron.cpp:35-43)
 template <int N, class HM>
-GA_FN double model(const double* g, const HM& h, const double* s) {
+GA_FN double model(const double* g, const HM& h, const double* s, double* gs_out = nullptr) {
     double q = vdot<N>(g, s);
+    if (gs_out) *gs_out = q;  // g's, reused by the Cauchy decrease test
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         double hs = 0.0;
@@ -224,12 +225,17 @@ GA_FN void cauchy_point(const double* x, const double* g, const HM& h,
     // tron_step's qc = q(s) (tron.cpp:278) reuses it (same inputs, same bits)
     double mt = 0.0;
     bool mt_ok = false;
+    // ||t|| <= delta as t.t <= bound (exact, ga_math.h); the model value is
+    // computed regardless (independent chains overlap, no branch), and used
+    // only when the radius test passes, as in the reference's order.
+    bool bound_ok;
+    const double dd_max = sqrt_le_bound(delta, &bound_ok);
     auto ok = [&](const double* st) {
-        mt_ok = false;
-        if (!(vnorm2<N, kOol>(st) <= delta)) return false;
-        mt = model<N>(g, h, st);
-        mt_ok = true;
-        return mt <= kTronMu0 * vdot<N>(g, st);
+        const double dd = vdot<N>(st, st);
+        double gs;
+        mt = model<N>(g, h, st, &gs);
+        mt_ok = bound_ok ? dd <= dd_max : tsqrt<kOol>(dd) <= delta;
+        return mt_ok && mt <= kTronMu0 * gs;
     };
     // One trial site (instruction-cache footprint: this is the hottest loop of
     // the lane phase, ~21 trials per step): phase 0 is alpha0, phase 1 the
@@ -483,6 +489,8 @@ struct TileSearch {
             return;
         }
         const double alpha0 = smin(1.0, delta / gnorm);
+        bool bound_ok;
+        const double dd_max = sqrt_le_bound(delta, &bound_ok);
         double mys[N];
         // One trial site and one broadcast site (code size: this runs in a
         // persistent kernel whose hot loop must stay in the instruction cache).
@@ -505,11 +513,11 @@ struct TileSearch {
                 for (int k = 0; k < -c; ++k) a *= 0.5;
 #pragma unroll
                 for (int i = 0; i < N; ++i) mys[i] = sclamp(x[i] - a * g[i], l[i], u[i]) - x[i];
-                if (vnorm2<N>(mys) <= delta) {
-                    mv = model<N>(g, h, mys);
-                    mok = true;
-                    okc = mv <= kTronMu0 * vdot<N>(g, mys);
-                }
+                const double dd = vdot<N>(mys, mys);
+                double gs;
+                mv = model<N>(g, h, mys, &gs);
+                mok = bound_ok ? dd <= dd_max : tsqrt<true>(dd) <= delta;  // (out of range: never in practice)
+                okc = mok && mv <= kTronMu0 * gs;
             }
             const unsigned okm = ballot(okc);
             int src = -1;      // lane whose trial step becomes s

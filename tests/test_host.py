@@ -48,6 +48,23 @@ def test_c_program_links_against_library(gridadmm, tmp_path):
     assert out.returncode == 0 and out.stdout.strip() == "ok", (out.returncode, out.stdout, out.stderr)
 
 
+def test_sqrt_le_bound_is_exact(tmp_path):
+    """The compare-only trust-region test of the Cauchy search
+    (ga_math.h sqrt_le_bound): y <= t(d) iff sqrt(y) <= d, t(d) maximal, on
+    4M random radii across the exponent range and every y within 6 ulps of
+    d*d; out-of-range and special radii fall back to the square root."""
+    import subprocess
+    exe = tmp_path / "sqrt_bound_check"
+    src = os.path.join(REPO, "tests", "c", "sqrt_bound_check.cpp")
+    inc = os.path.join(REPO, "paper_2110_06879_b200", "csrc")
+    r = subprocess.run(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-I", inc, src, "-o", str(exe)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(exe), "4000000"], capture_output=True, text=True)
+    fails, checked = map(int, out.stdout.split())
+    assert fails == 0 and checked > 3_000_000
+
+
 def test_network_dimensions_and_errors(gridadmm):
     net = gridadmm.Network(case_path("case9"))
     assert (net.num_buses, net.num_generators, net.num_branches) == (9, 3, 9)

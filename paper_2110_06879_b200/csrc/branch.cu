@@ -70,7 +70,10 @@ constexpr double kAlTol = 1e-8;
 constexpr double kAlShrink = 0.25;
 constexpr double kRhoTildeMax = 1e7;
 
-constexpr int kLaneBlock = 256;  // lane phase: one slot per thread (64 / 128 / 256 per block:
+#ifndef GA_LANE_BLOCK
+#define GA_LANE_BLOCK 256
+#endif
+constexpr int kLaneBlock = GA_LANE_BLOCK;  // lane phase: one slot per thread (64 / 128 / 256 per block:
                                  // 7.05 / 7.05 / 6.99 s on the full 70k solve)
 constexpr int kTileBlock = 128;  // tile phase: one slot per tile
 constexpr int kTile = 4;  // lanes per branch in the tile phase (full 70k solve: 2 / 4 / 8 / 16

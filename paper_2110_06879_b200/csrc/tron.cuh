@@ -205,6 +205,15 @@ GA_FN double boundary_tau(const double* s, const double* p, double delta) {
     return tdiv<kOol>(-sp + tsqrt<kOol>(disc), pp);
 }
 
+// l <= x <= u componentwise (false on NaN).
+template <int N>
+GA_FN bool box_contains(const double* x, const double* l, const double* u) {
+    bool in = true;
+#pragma unroll
+    for (int i = 0; i < N; ++i) in = in && l[i] <= x[i] && x[i] <= u[i];
+    return in;
+}
+
 // Cauchy point (tron.cpp:101-137).
 template <int N, bool kOol, class HM>
 GA_FN void cauchy_point(const double* x, const double* g, const HM& h,
@@ -230,11 +239,21 @@ GA_FN void cauchy_point(const double* x, const double* g, const HM& h,
     // only when the radius test passes, as in the reference's order.
     bool bound_ok;
     const double dd_max = sqrt_le_bound(delta, &bound_ok);
-    auto ok = [&](const double* st) {
-        const double dd = vdot<N>(st, st);
+    // A backtracking trial at alpha0 * 2^-k, k >= 2, passes the radius test
+    // for sure when x is inside its box: |t_i| <= 2 alpha |g_i| (1+u)^2
+    // (fl(x - alpha g_i) is at least as close to x - alpha g_i as x is, the
+    // clamp only moves it toward x), alpha0 ||g|| <= delta (1+10u), so the
+    // computed ||t|| <= delta (1+20u) / 2 < delta — the test is skipped.
+    const bool in_box = box_contains<N>(x, l, u);
+    auto ok = [&](const double* st, bool sure) {
         double gs;
         mt = model<N>(g, h, st, &gs);
-        mt_ok = bound_ok ? dd <= dd_max : tsqrt<kOol>(dd) <= delta;
+        if (sure) {
+            mt_ok = true;
+        } else {
+            const double dd = vdot<N>(st, st);
+            mt_ok = bound_ok ? dd <= dd_max : tsqrt<kOol>(dd) <= delta;
+        }
         return mt_ok && mt <= kTronMu0 * gs;
     };
     // One trial site (instruction-cache footprint: this is the hottest loop of
@@ -247,7 +266,7 @@ GA_FN void cauchy_point(const double* x, const double* g, const HM& h,
     double t[N];
     for (;;) {
         step_at(a, t);
-        const bool o = ok(t);
+        const bool o = ok(t, in_box && phase == 2 && cnt >= 2);
         if (phase == 0) {
             phase = o ? 1 : 2;
         } else if (phase == 1) {
@@ -491,6 +510,8 @@ struct TileSearch {
         const double alpha0 = smin(1.0, delta / gnorm);
         bool bound_ok;
         const double dd_max = sqrt_le_bound(delta, &bound_ok);
+        const bool in_box = box_contains<N>(x, l, u);  // trials at c <= -2: radius test
+                                                        // passes (cauchy_point)
         double mys[N];
         // One trial site and one broadcast site (code size: this runs in a
         // persistent kernel whose hot loop must stay in the instruction cache).
@@ -513,10 +534,14 @@ struct TileSearch {
                 for (int k = 0; k < -c; ++k) a *= 0.5;
 #pragma unroll
                 for (int i = 0; i < N; ++i) mys[i] = sclamp(x[i] - a * g[i], l[i], u[i]) - x[i];
-                const double dd = vdot<N>(mys, mys);
                 double gs;
                 mv = model<N>(g, h, mys, &gs);
-                mok = bound_ok ? dd <= dd_max : tsqrt<true>(dd) <= delta;  // (out of range: never in practice)
+                if (in_box && c <= -2) {
+                    mok = true;
+                } else {
+                    const double dd = vdot<N>(mys, mys);
+                    mok = bound_ok ? dd <= dd_max : tsqrt<true>(dd) <= delta;  // (out of range: never in practice)
+                }
                 okc = mok && mv <= kTronMu0 * gs;
             }
             const unsigned okm = ballot(okc);

@@ -65,6 +65,23 @@ def test_sqrt_le_bound_is_exact(tmp_path):
     assert fails == 0 and checked > 3_000_000
 
 
+def test_cauchy_radius_skip_is_sound(tmp_path):
+    """The Cauchy search skips the radius test of backtracking trials at
+    alpha0 * 2^-k, k >= 2, when x is inside its box (tron.cuh cauchy_point):
+    on 2M random / adversarial instances that test always passes, while at
+    k = 0 it fails often (the checker reaches the boundary)."""
+    import subprocess
+    exe = tmp_path / "cauchy_radius_check"
+    src = os.path.join(REPO, "tests", "c", "cauchy_radius_check.cpp")
+    inc = os.path.join(REPO, "paper_2110_06879_b200", "csrc")
+    r = subprocess.run(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-I", inc, src, "-o", str(exe)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(exe), "2000000"], capture_output=True, text=True)
+    viol, k0_fail, n = map(int, out.stdout.split())
+    assert viol == 0 and n == 2_000_000 and k0_fail > 10_000
+
+
 def test_network_dimensions_and_errors(gridadmm):
     net = gridadmm.Network(case_path("case9"))
     assert (net.num_buses, net.num_generators, net.num_branches) == (9, 3, 9)

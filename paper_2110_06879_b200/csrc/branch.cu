@@ -90,6 +90,7 @@ struct Work {
     int* solo6;
     int* solo4;
     int* ctr;
+    unsigned char* defer;  // [nb] bus adjacent to a branch handed on by the lane phase
 };
 
 Work work_of(const DevNet& n, const DevState& s) {
@@ -99,6 +100,7 @@ Work work_of(const DevNet& n, const DevState& s) {
     w.solo6 = w.ovf4 + n.n_unl;
     w.solo4 = w.solo6 + n.n_lim;
     w.ctr = w.solo4 + n.n_unl;
+    w.defer = reinterpret_cast<unsigned char*>(w.ctr + kCounters);
     return w;
 }
 
@@ -207,7 +209,8 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
                                         const BranchCfg& cfg, const int* list, int count,
                                         int* cursor, int* ovf, int* ovf_count, double* smem,
                                         unsigned long long* iters_out, int* fail_out,
-                                        unsigned long long* exec_dst, int* done_ctr) {
+                                        unsigned long long* exec_dst, int* done_ctr,
+                                        unsigned char* defer) {
     constexpr unsigned kFull = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     unsigned my_exec = 0;  // trust-region steps executed by this lane
@@ -301,6 +304,9 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
                 st.br_cost[b] = steps;
 #endif
                 ovf[atomicAdd(ovf_count, 1)] = b;
+                // its end buses wait for the tile / solo phases (bus kernel split)
+                defer[net.br_from[b]] = 1;
+                defer[net.br_to[b]] = 1;
                 atomicAdd(done_ctr, 1);
                 b = -1;
             }
@@ -332,14 +338,14 @@ __global__ void __launch_bounds__(kLaneBlock, GA_LANE_MINB) lane_kernel(DevNet n
     // so each SM's warps share one code path (instruction-cache locality).
     if ((sm_id() & 1u) == 0) {
         lane_phase<6>(net, st, cfg, net.lim_list, net.n_lim, &w.ctr[0], w.ovf6, &w.ctr[2], smem,
-                      &it6, &fails, &sc->exec6, &w.ctr[10]);
+                      &it6, &fails, &sc->exec6, &w.ctr[10], w.defer);
         lane_phase<4>(net, st, cfg, net.unl_list, net.n_unl, &w.ctr[1], w.ovf4, &w.ctr[3], smem,
-                      &it4, &fails, &sc->exec4, &w.ctr[11]);
+                      &it4, &fails, &sc->exec4, &w.ctr[11], w.defer);
     } else {
         lane_phase<4>(net, st, cfg, net.unl_list, net.n_unl, &w.ctr[1], w.ovf4, &w.ctr[3], smem,
-                      &it4, &fails, &sc->exec4, &w.ctr[11]);
+                      &it4, &fails, &sc->exec4, &w.ctr[11], w.defer);
         lane_phase<6>(net, st, cfg, net.lim_list, net.n_lim, &w.ctr[0], w.ovf6, &w.ctr[2], smem,
-                      &it6, &fails, &sc->exec6, &w.ctr[10]);
+                      &it6, &fails, &sc->exec6, &w.ctr[10], w.defer);
     }
     const unsigned full = 0xffffffffu;
 #pragma unroll
@@ -685,8 +691,10 @@ int persistent_blocks(K kernel, int block, size_t smem) {
 }  // namespace
 
 size_t branch_workspace_ints(const DevNet& n) {
-    return 2 * (static_cast<size_t>(n.n_lim) + n.n_unl) + kCounters;
+    return 2 * (static_cast<size_t>(n.n_lim) + n.n_unl) + kCounters + (static_cast<size_t>(n.nb) + 3) / 4;
 }
+
+unsigned char* bus_defer_flags(const DevNet& n, const DevState& s) { return work_of(n, s).defer; }
 
 const int* branch_overflow_counts(const DevNet& n, const DevState& s) {
     return work_of(n, s).ctr + 2;
@@ -719,7 +727,7 @@ const Grids& branch_grids() {
 void prepare_branch_launch() { (void)branch_grids(); }
 
 void launch_branches(const DevNet& n, const DevState& s, const BranchCfg& cfg, DevScalars* sc,
-                     cudaStream_t st, cudaEvent_t mid) {
+                     cudaStream_t st, cudaEvent_t mid, const std::function<void()>& after_lane) {
     if (n.nl <= 0) return;
     const Work w = work_of(n, s);
     cudaMemsetAsync(w.ctr, 0, kCounters * sizeof(int), st);
@@ -740,6 +748,7 @@ void launch_branches(const DevNet& n, const DevState& s, const BranchCfg& cfg, D
     lane_kernel<<<lane_blocks < need ? lane_blocks : need, kLaneBlock, lane_smem, st>>>(n, s, lc,
                                                                                        w, sc);
     if (mid) cudaEventRecord(mid, st);
+    if (after_lane) after_lane();
     tile_kernel<<<tile_blocks, kTileBlock, 0, st>>>(n, s, cfg, w, sc);
     if (cfg.tile_budget > 0) solo_kernel<<<solo_blocks, kSoloBlock, 0, st>>>(n, s, cfg, w, sc);
 }

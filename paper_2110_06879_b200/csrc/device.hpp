@@ -21,6 +21,7 @@
 #include <cstdint>
 
 #include <cuda_runtime.h>
+#include <functional>
 
 namespace ga {
 
@@ -165,7 +166,11 @@ void launch_extract(const DevNet& n, const DevState& s, const DevExtract& e, cud
 void launch_generators(const DevNet& n, const DevState& s, cudaStream_t st);
 // `mid` (optional) is recorded between the lane-phase and tile-phase kernels.
 void launch_branches(const DevNet& n, const DevState& s, const BranchCfg& cfg,
-                     DevScalars* sc, cudaStream_t st, cudaEvent_t mid = nullptr);
+                     DevScalars* sc, cudaStream_t st, cudaEvent_t mid = nullptr,
+                     const std::function<void()>& after_lane = {});
+// Per-bus flags set by the lane kernel for the end buses of every branch it
+// hands on to the tile / solo phases (cleared by the caller per iteration).
+unsigned char* bus_defer_flags(const DevNet& n, const DevState& s);
 // One-time launch setup of the branch kernels (grid sizes, smem attribute);
 // called before a stream capture, where such calls are not allowed.
 void prepare_branch_launch();
@@ -175,8 +180,12 @@ void launch_buses(const DevNet& n, const DevState& s, DevScalars* sc, cudaStream
 // Bus QP fused with the generator projection, z, y and all four residual
 // norms (the iteration path).  With a gate (graph path) beta is read from
 // gate->beta and the launch is a no-op once gate->stop is set.
+// sel: 0 every bus; 1 the buses whose flag in `defer` is clear; 2 the
+// flagged ones.  Buses are independent and the norms order-free maxima, so
+// 1 then 2 is the same as 0 (the split lets 1 run beside the tile phase).
 void launch_bus_zy(const DevNet& n, const DevState& s, double beta, DevScalars* sc,
-                   cudaStream_t st, LoopCtl* gate = nullptr);
+                   cudaStream_t st, LoopCtl* gate = nullptr,
+                   const unsigned char* defer = nullptr, int sel = 0);
 // Graph path: stamp the loop start and clear the scalars / the control
 // kernel after each iteration (records, stop tests, scalar reset).
 void launch_loop_start(LoopCtl* ctl, DevScalars* sc, cudaStream_t st);

@@ -235,13 +235,14 @@ __device__ __forceinline__ unsigned long long global_ns() {
     return t;
 }
 
-template <bool kZY, int kTPB>
+template <bool kZY, int kTPB, int kSel = 0>
 __global__ void __launch_bounds__(kTPB * kBB) bus_block_kernel(DevNet n, DevState s, double beta,
-                                                       DevScalars* sc, LoopCtl* gate) {
+                                                       DevScalars* sc, LoopCtl* gate,
+                                                       const unsigned char* defer = nullptr) {
     if (gate) {
         if (*reinterpret_cast<volatile int*>(&gate->stop)) return;
         beta = gate->beta;
-        if (blockIdx.x == 0 && threadIdx.x == 0) gate->t_bus = global_ns();
+        if (kSel != 1 && blockIdx.x == 0 && threadIdx.x == 0) gate->t_bus = global_ns();
     }
     __shared__ int s_off[kBB + 1];
     __shared__ int s_base[kBB];       // segment start (storage position) of each slot's bus
@@ -257,8 +258,10 @@ __global__ void __launch_bounds__(kTPB * kBB) bus_block_kernel(DevNet n, DevStat
     int i = -1, cnt = 0, ge = 0, qs = 0;
     {
         int start = 0;
-        if (tid < kBB && t < nbus) {
-            i = n.bus_at(t);
+        if (tid < kBB && t < nbus) i = n.bus_at(t);
+        // a bus outside this launch's selection owns no rows here (cnt 0)
+        if (kSel != 0 && i >= 0 && (defer[i] != 0) != (kSel == 2)) i = -1;
+        if (i >= 0) {
             const int* seg = n.bus_seg + 4 * i;
             start = __ldg(seg);
             ge = __ldg(seg + 1) - start;
@@ -762,14 +765,22 @@ void launch_buses(const DevNet& n, const DevState& s, DevScalars* sc, cudaStream
 }
 
 void launch_bus_zy(const DevNet& n, const DevState& s, double beta, DevScalars* sc,
-                   cudaStream_t st, LoopCtl* gate) {
+                   cudaStream_t st, LoopCtl* gate, const unsigned char* defer, int sel) {
     const int c = n.buses_count();
     if (c <= 0) return;
     const int blocks = (c + kBB - 1) / kBB;
-    if (bus_two_threads(blocks))
-        bus_block_kernel<true, 2><<<blocks, 2 * kBB, 0, st>>>(n, s, beta, sc, gate);
-    else
-        bus_block_kernel<true, 1><<<blocks, kBB, 0, st>>>(n, s, beta, sc, gate);
+#define GA_BUS_SEL(TPB)                                                                          \
+    switch (sel) {                                                                               \
+        case 1: bus_block_kernel<true, TPB, 1><<<blocks, TPB * kBB, 0, st>>>(n, s, beta, sc, gate, defer); break; \
+        case 2: bus_block_kernel<true, TPB, 2><<<blocks, TPB * kBB, 0, st>>>(n, s, beta, sc, gate, defer); break; \
+        default: bus_block_kernel<true, TPB, 0><<<blocks, TPB * kBB, 0, st>>>(n, s, beta, sc, gate, nullptr); \
+    }
+    if (bus_two_threads(blocks)) {
+        GA_BUS_SEL(2)
+    } else {
+        GA_BUS_SEL(1)
+    }
+#undef GA_BUS_SEL
 }
 
 void launch_z_only(const DevNet& n, const DevState& s, double beta, cudaStream_t st) {

@@ -198,6 +198,12 @@ public:
     // rho_max), z_inf, z_drift; returns branch failures; throws
     // SingularBusError.
     int iterate(double out[4], PhaseTimes* times) override { return iterate_ev(out, times, nullptr); }
+    // One inner iteration's branch and bus kernels on stream_: the bus kernel
+    // for the buses not adjacent to a branch still running after the lane
+    // phase runs on side_ beside the tile / solo phases, the rest after them
+    // (GRIDADMM_BUS_OVERLAP=0: one bus kernel after the branch phase).
+    void enqueue_iteration(const BranchCfg& bc, LoopCtl* gate, cudaEvent_t mid,
+                           cudaEvent_t before_bus);
     int iterate_ev(double out[4], PhaseTimes* times, cudaEvent_t end_event);
 
     // Benchmark helper: k iterations, each bracketed by CUDA events on the
@@ -248,6 +254,10 @@ private:
     size_t flush_size_ = 0;
     double beta_ = 0.0;
     cudaStream_t stream_ = nullptr;
+    cudaStream_t side_ = nullptr;  // bus kernel (undeferred buses) beside the tile / solo phases
+    cudaEvent_t fork_ = nullptr, join_ = nullptr;
+    cudaEvent_t side_ev_[2] = {};  // bus kernel on side_ (timed iterations)
+    bool side_timed_ = false;      // the last timed iteration split the bus kernel
     cudaEvent_t ev_[6] = {};
     KernelClock clocks_[6];  // gen, branch, bus(+z/y), zy (fused: 0), lane phase, tile phase
     std::FILE* prof_ = nullptr;  // GRIDADMM_PROFILE=<csv>: per-iteration kernel times

@@ -4,8 +4,10 @@
 set -x
 O=${O:-gpurun_out/ncu}
 mkdir -p $O
+# (the bus kernel unsplit, GRIDADMM_BUS_OVERLAP=0: one launch per iteration)
 for k in ${KERNELS:-lane_kernel tile_kernel bus_block_kernel}; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 10 -c 1 \
+  ov=1; [ $k = bus_block_kernel ] && ov=0
+  GRIDADMM_BUS_OVERLAP=$ov timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 10 -c 1 \
       -o $O/$k -f python scripts/ncu_target.py case_ACTIVSg70k 12 > $O/$k.log 2>&1
 done
 timeout 900 ncu --clock-control none --csv -k regex:"lane_kernel|tile_kernel|solo_kernel" \

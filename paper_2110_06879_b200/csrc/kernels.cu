@@ -775,7 +775,12 @@ void launch_bus_zy(const DevNet& n, const DevState& s, double beta, DevScalars* 
         case 2: bus_block_kernel<true, TPB, 2><<<blocks, TPB * kBB, 0, st>>>(n, s, beta, sc, gate, defer); break; \
         default: bus_block_kernel<true, TPB, 0><<<blocks, TPB * kBB, 0, st>>>(n, s, beta, sc, gate, nullptr); \
     }
-    if (bus_two_threads(blocks)) {
+    // the flagged buses (sel 2) are a few per block: two threads per bus
+    // shorten their row phases whatever the grid size
+#ifndef GA_BUS_B_TPB2
+#define GA_BUS_B_TPB2 1
+#endif
+    if (bus_two_threads(blocks) || (GA_BUS_B_TPB2 && sel == 2)) {
         GA_BUS_SEL(2)
     } else {
         GA_BUS_SEL(1)

@@ -775,12 +775,9 @@ void launch_bus_zy(const DevNet& n, const DevState& s, double beta, DevScalars* 
         case 2: bus_block_kernel<true, TPB, 2><<<blocks, TPB * kBB, 0, st>>>(n, s, beta, sc, gate, defer); break; \
         default: bus_block_kernel<true, TPB, 0><<<blocks, TPB * kBB, 0, st>>>(n, s, beta, sc, gate, nullptr); \
     }
-    // the flagged buses (sel 2) are a few per block: two threads per bus
-    // shorten their row phases whatever the grid size
-#ifndef GA_BUS_B_TPB2
-#define GA_BUS_B_TPB2 1
-#endif
-    if (bus_two_threads(blocks) || (GA_BUS_B_TPB2 && sel == 2)) {
+    // (two threads per bus for the sel-2 launch alone, whose blocks hold a
+    // few flagged buses each: 33.4 vs 27.8 us, profiles/ab/r02_bus_overlap_b_tpb2.jsonl)
+    if (bus_two_threads(blocks)) {
         GA_BUS_SEL(2)
     } else {
         GA_BUS_SEL(1)

@@ -35,11 +35,14 @@ rows = np.genfromtxt(prof, delimiter=",", names=True)
 m = rep.metrics()
 n = len(rows)
 dev = {k: float(np.sum(rows[k])) * 1e-3 for k in ("gen_ms", "lane_ms", "tile_ms", "bus_zy_ms")}
-dev_total = sum(dev.values())
+dev_total = sum(dev.values())  # the critical path: the side-stream bus launch overlaps tile_ms
+if "bus_side_ms" in rows.dtype.names:
+    dev["bus_side_ms_overlapped"] = float(np.sum(rows["bus_side_ms"])) * 1e-3
 deciles = []
 for q in range(10):
     part = rows[q * n // 10:(q + 1) * n // 10]
-    deciles.append({k: float(np.mean(part[k])) for k in ("lane_ms", "tile_ms", "bus_zy_ms")})
+    deciles.append({k: float(np.mean(part[k])) for k in ("lane_ms", "tile_ms", "bus_zy_ms")
+                    + (("bus_side_ms",) if "bus_side_ms" in rows.dtype.names else ())})
 out = {"shape": shape, "preset": preset, "status": ga.STATUS[st], "wall_s": wall,
        "inner_iterations": int(m["inner_iterations"]), "c_inf": m["c_inf"],
        "device_s": dev, "device_total_s": dev_total, "host_gap_s": wall - dev_total,

@@ -71,6 +71,14 @@ gridadmm_status gridadmm_network_export(const gridadmm_network* net, double* bus
 gridadmm_status gridadmm_network_partition(const gridadmm_network* net, int k,
                                            int* part_of_bus);
 
+/* Per-branch work weights for the partition above (e.g. the TRON steps of
+ * a previous sweep from gridadmm_session_branch_costs, so the heavy-tailed
+ * branches spread over the parts): weights[b] >= 0 for every branch, or NULL
+ * to restore the class weights.  Every rank of a multi-process run must set
+ * the same weights before creating its session.  Results never depend on
+ * the partition. */
+gridadmm_status gridadmm_network_set_branch_weights(gridadmm_network* net, const int* weights);
+
 /* Exchange plan of part p of the k-way partition (host only): the rows
  * whose x part p sends to peer q after the branch phase (and whose xbar, z,
  * y it gets back after the bus phase), and the rows whose x it receives from

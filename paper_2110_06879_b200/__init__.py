@@ -79,6 +79,7 @@ EXT_SYMBOLS = {
     "gridadmm_network_export": (_I, [_P, _DP, _IP, _DP, _IP, _DP, _IP]),
     "gridadmm_network_layout": (_I, [_P, _IP, _IP]),
     "gridadmm_network_partition": (_I, [_P, _I, _IP]),
+    "gridadmm_network_set_branch_weights": (_I, [_P, _IP]),
     "gridadmm_network_exchange_rows": (_I, [_P, _I, _I, _I, _IP, _IP, _IP, _IP]),
     "gridadmm_session_new": (_I, [_P, _P, ctypes.POINTER(_P)]),
     "gridadmm_session_free": (None, [_P]),
@@ -200,6 +201,18 @@ class Network:
         out = np.zeros(max(1, self.num_buses), dtype=np.int32)
         _check(lib().gridadmm_network_partition(self._h, k, out.ctypes.data_as(_IP)))
         return out[: self.num_buses]
+
+    def set_branch_weights(self, weights) -> None:
+        """Per-branch partition weights, e.g. Session.branch_costs() of a
+        previous sweep (gridadmm_network_set_branch_weights); None restores
+        the class weights."""
+        if weights is None:
+            _check(lib().gridadmm_network_set_branch_weights(self._h, None))
+            return
+        w = np.ascontiguousarray(weights, dtype=np.int32)
+        if w.shape != (self.num_branches,):
+            raise ValueError("one weight per branch")
+        _check(lib().gridadmm_network_set_branch_weights(self._h, w.ctypes.data_as(_IP)))
 
     def exchange_rows(self, k: int, p: int, q: int):
         """(send, recv) row lists of part p toward peer q (gridadmm_network_exchange_rows)."""

@@ -203,6 +203,21 @@ gridadmm_status gridadmm_network_partition(const gridadmm_network* n, int k, int
     return GRIDADMM_OK;
 }
 
+gridadmm_status gridadmm_network_set_branch_weights(gridadmm_network* n, const int* weights) {
+    if (!n) return fail(GRIDADMM_ERR_INVALID_ARG, "null network");
+    if (!weights) {
+        n->net.branch_weight.clear();
+        return GRIDADMM_OK;
+    }
+    const int nl = n->net.nl();
+    for (int b = 0; b < nl; ++b)
+        if (weights[b] < 0) return fail(GRIDADMM_ERR_INVALID_ARG, "negative branch weight");
+    return guarded([&]() -> gridadmm_status {
+        n->net.branch_weight.assign(weights, weights + nl);
+        return GRIDADMM_OK;
+    });
+}
+
 gridadmm_status gridadmm_network_exchange_rows(const gridadmm_network* n, int k, int p, int q,
                                                int* send_rows, int* n_send, int* recv_rows,
                                                int* n_recv) {

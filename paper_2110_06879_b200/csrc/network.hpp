@@ -52,6 +52,9 @@ struct Network {
     std::vector<Line> lines;
     std::unordered_map<int, int> bus_index;
     int ref_bus = -1;
+    // optional per-branch work weights for the bus partition (e.g. measured
+    // TRON steps, gridadmm_session_branch_costs); empty = class weights
+    std::vector<int> branch_weight;
 
     int nb() const { return static_cast<int>(buses.size()); }
     int ng() const { return static_cast<int>(gens.size()); }

@@ -12,16 +12,19 @@ std::vector<int> partition_buses(const Network& net, int k) {
     if (k <= 1 || nb == 0) return part;
     // adjacency in ascending neighbour order
     std::vector<std::vector<int>> adj(nb);
-    std::vector<int> weight(nb, 1);
+    std::vector<long long> weight(nb, 1);
+    const bool measured = static_cast<int>(net.branch_weight.size()) == nl;
     for (int b = 0; b < nl; ++b) {
         const int f = net.lines[b].from, t = net.lines[b].to;
         adj[f].push_back(t);
         adj[t].push_back(f);
-        // a branch is solved on its from-bus part (the dominant work); a
-        // rate-limited branch (6 variables + the AL loop) costs about twice
-        // an unlimited one per TRON iteration (census) and runs
-        // the AL tails, so it weighs double
-        weight[f] += net.lines[b].limited() ? 8 : 4;
+        // a branch is solved on its from-bus part (the dominant work).  With
+        // measured weights (TRON steps of a previous sweep) the heavy-tailed
+        // branches spread over the parts; otherwise a rate-limited branch (6
+        // variables + the AL loop) costs about twice an unlimited one per
+        // TRON iteration (census) and runs the AL tails
+        if (measured) weight[f] += 1 + static_cast<long long>(net.branch_weight[b]);
+        else weight[f] += net.lines[b].limited() ? 8 : 4;
     }
     for (auto& a : adj) std::sort(a.begin(), a.end());
     std::vector<int> order;
@@ -44,7 +47,7 @@ std::vector<int> partition_buses(const Network& net, int k) {
         }
     }
     long long total = 0;
-    for (int w : weight) total += w;
+    for (long long w : weight) total += w;
     long long acc = 0;
     for (int u : order) {
         int p = static_cast<int>((acc * k) / std::max<long long>(total, 1));

@@ -31,7 +31,8 @@ struct PartPlan {
 };
 
 // part[i] for every bus: BFS order from bus 0 over the branch graph (ties by
-// index), cut into k contiguous chunks balancing owned branch work.  Parts
+// index), cut into k contiguous chunks balancing owned branch work (class
+// weights, or net.branch_weight when set).  Parts
 // may be empty when k exceeds what the graph can fill.
 std::vector<int> partition_buses(const Network& net, int k);
 

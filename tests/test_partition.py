@@ -55,6 +55,33 @@ def test_partition_invariants(gridadmm, name, k):
             assert plans[p][0][q] == plans[q][1][p]
 
 
+def test_weighted_partition_balances_measured_cost(gridadmm):
+    """gridadmm_network_set_branch_weights: the contiguous BFS cut balances
+    1 per bus + (1 + w_b) per from-branch to within one bus's weight; NULL
+    restores the class weights; negative weights are rejected."""
+    net = gridadmm.Network(case_path("case118"))
+    k = 3
+    base = net.partition(k)
+    ex = net.export()
+    nl = net.num_branches
+    w = (np.random.default_rng(3).pareto(1.2, nl) * 8).astype(np.int32)
+    net.set_branch_weights(w)
+    part = net.partition(k)
+    assert np.array_equal(part, net.partition(k)) and not np.array_equal(part, base)
+    bus_w = np.ones(net.num_buses, dtype=np.int64)
+    for b, (f, _t) in enumerate(ex["ends"]):
+        bus_w[f] += 1 + int(w[b])
+    load = np.bincount(part, weights=bus_w, minlength=k)
+    assert load.max() <= bus_w.sum() / k + bus_w.max()
+    net.set_branch_weights(None)
+    assert np.array_equal(net.partition(k), base)
+    bad = w.copy()
+    bad[5] = -1
+    with pytest.raises(gridadmm.GridAdmmError) as e:
+        net.set_branch_weights(bad)
+    assert e.value.status == 3
+
+
 def _rank_main(rank, world, path, port, out):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"

@@ -50,7 +50,14 @@ def norms(s, xbar_prev, z_prev, rows):
                      np.max(np.abs(s["z"][rows] - z_prev[rows]), initial=0.0)])
 
 
-def _rank_main(rank, world, path, port, out):
+def heavy_tailed_weights(nl, seed=7):
+    """Per-branch weights shaped like measured TRON step counts (a few very
+    long chains), for the weighted partition."""
+    rng = np.random.default_rng(seed)
+    return (rng.pareto(1.2, nl) * 8).astype(np.int32)
+
+
+def _rank_main(rank, world, path, port, out, weights=None):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -61,6 +68,8 @@ def _rank_main(rank, world, path, port, out):
     import oracle
     import paper_2110_06879_b200 as ga
     net = ga.Network(path)
+    if weights is not None:
+        net.set_branch_weights(weights)
     ex = net.export()
     part = net.partition(world)
     row_owner, br_owner, bus_owner = ownership(ex, part)
@@ -118,19 +127,26 @@ def _rank_main(rank, world, path, port, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,world", [("case118", 2), ("case118", 3), ("case30", 2)])
-def test_exchange_protocol_bit_identical(gridadmm, oracle_mod, name, world):
+@pytest.mark.parametrize("name,world,weighted", [("case118", 2, False), ("case118", 3, False),
+                                                 ("case30", 2, False), ("case118", 3, True)])
+def test_exchange_protocol_bit_identical(gridadmm, oracle_mod, name, world, weighted):
     import torch.multiprocessing as mp
     path = case_path(name)
+    net = gridadmm.Network(path)
+    weights = None
+    if weighted:  # measured-cost partition (gridadmm_network_set_branch_weights)
+        unweighted = net.partition(world)
+        weights = heavy_tailed_weights(net.num_branches)
+        net.set_branch_weights(weights)
+        assert not np.array_equal(net.partition(world), unweighted)
     sock = socket.socket()
     sock.bind(("127.0.0.1", 0))
     port = sock.getsockname()[1]
     sock.close()
     out = mp.Manager().dict()
-    mp.spawn(_rank_main, args=(world, path, port, out), nprocs=world, join=True)
+    mp.spawn(_rank_main, args=(world, path, port, out, weights), nprocs=world, join=True)
 
     # single process, same phases
-    net = gridadmm.Network(path)
     ex = net.export()
     part = net.partition(world)
     row_owner, br_owner, bus_owner = ownership(ex, part)

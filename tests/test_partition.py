@@ -139,6 +139,29 @@ def test_partitioned_iterations_bit_identical(gridadmm, name, k):
 
 
 @pytest.mark.gpu
+def test_partition_by_measured_branch_costs_bit_identical(gridadmm):
+    """Partition weighted by the TRON steps a first sweep measured
+    (Session.branch_costs -> Network.set_branch_weights): the 3-part run
+    stays bit-identical to one part."""
+    net = gridadmm.Network(case_path("case118"))
+    s1 = gridadmm.Session(net, gridadmm.Config("case118", eps=1e-5))
+    s1.iterate(5)
+    cost = np.asarray(s1.branch_costs(), dtype=np.int64)
+    assert cost.shape == (net.num_branches,) and cost.max() > 0
+    base = net.partition(3)
+    net.set_branch_weights(np.minimum(cost, 1 << 20).astype(np.int32))
+    assert not np.array_equal(net.partition(3), base)
+    s1 = gridadmm.Session(net, gridadmm.Config("case118", eps=1e-5))
+    s3 = gridadmm.Session(net, gridadmm.Config("case118", eps=1e-5, partitions=3))
+    r1, _ = s1.iterate(60)
+    r3, _ = s3.iterate(60)
+    assert np.array_equal(r1.view(np.uint64), r3.view(np.uint64))
+    a, b = s1.get_state(), s3.get_state()
+    for f in a:
+        assert np.array_equal(a[f].view(np.uint64), b[f].view(np.uint64)), f
+
+
+@pytest.mark.gpu
 def test_partitioned_full_solve_case9(gridadmm):
     net = gridadmm.Network(case_path("case9"))
     st1, r1 = gridadmm.solve(net, gridadmm.Config("case9", eps=1e-5))

@@ -259,10 +259,8 @@ __global__ void __launch_bounds__(kTPB * kBB) bus_block_kernel(DevNet n, DevStat
     {
         int start = 0;
         if (tid < kBB && t < nbus) i = n.bus_at(t);
-        // a bus outside this launch's selection owns no rows here (cnt 0);
-        // a block left with none ends at once (its norms would be 0)
+        // a bus outside this launch's selection owns no rows here (cnt 0)
         if (kSel != 0 && i >= 0 && (defer[i] != 0) != (kSel == 2)) i = -1;
-        if (kSel != 0 && !__syncthreads_or(i >= 0)) return;
         if (i >= 0) {
             const int* seg = n.bus_seg + 4 * i;
             start = __ldg(seg);

@@ -179,6 +179,8 @@ __device__ __forceinline__ void finalize_branch(const DevNet& net, const DevStat
     double fl[4];
     branch_flows(YcView<S>{slot}, pt[0], pt[1], pt[2], pt[3], fl);
     // the from-quad (pij, qij, wi, thi) and the to-quad (pji, qji, wj, thj)
+    GA_CHECK(net.qpos[2 * b] >= 0 && net.qpos[2 * b] + 4 <= net.mpad);
+    GA_CHECK(net.qpos[2 * b + 1] >= 0 && net.qpos[2 * b + 1] + 4 <= net.mpad);
     double2* xf = reinterpret_cast<double2*>(st.x + net.qpos[2 * b]);
     double2* xt = reinterpret_cast<double2*>(st.x + net.qpos[2 * b + 1]);
     xf[0] = make_double2(fl[0], fl[1]);
@@ -246,6 +248,7 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
                 const int idx = base + __popc(need & ((1u << lane) - 1u));
                 if (idx < count) {
                     b = list[idx];
+                    GA_CHECK(b >= 0 && b < net.nl);
                     load_slot<kLaneBlock>(net, st, cfg, b, slot);
 #pragma unroll
                     for (int k = 0; k < N; ++k) ts.x[k] = st.bp[k * net.nl + b];
@@ -303,8 +306,12 @@ __device__ __noinline__ void lane_phase(const DevNet& net, const DevState& st,
 #if defined(GA_TRON_STATS) || defined(GA_BRANCH_STEPS)
                 st.br_cost[b] = steps;
 #endif
-                ovf[atomicAdd(ovf_count, 1)] = b;
+                const int slot_o = atomicAdd(ovf_count, 1);
+                GA_CHECK(slot_o >= 0 && slot_o < count);
+                ovf[slot_o] = b;
                 // its end buses wait for the tile / solo phases (bus kernel split)
+                GA_CHECK(net.br_from[b] >= 0 && net.br_from[b] < net.nb);
+                GA_CHECK(net.br_to[b] >= 0 && net.br_to[b] < net.nb);
                 defer[net.br_from[b]] = 1;
                 defer[net.br_to[b]] = 1;
                 atomicAdd(done_ctr, 1);
@@ -392,6 +399,7 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
         idx = __shfl_sync(mask, idx, 0, T);
         if (idx >= count) break;
         const int b = ovf[idx];
+        GA_CHECK(b >= 0 && b < net.nl);
         load_slot<S>(net, st, cfg, b, slot);
         TronState<N> ts;
 #pragma unroll
@@ -425,7 +433,9 @@ __device__ __noinline__ void tile_phase(const DevNet& net, const DevState& st,
 #if defined(GA_TRON_STATS) || defined(GA_BRANCH_STEPS)
                     st.br_cost[b] += (int)branch_exec;
 #endif
-                    solo[atomicAdd(solo_count, 1)] = b;
+                    const int slot_s = atomicAdd(solo_count, 1);
+                    GA_CHECK(slot_s >= 0 && slot_s < count);
+                    solo[slot_s] = b;
                 }
                 handed_off = true;
                 break;

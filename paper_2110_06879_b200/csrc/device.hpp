@@ -23,6 +23,18 @@
 #include <cuda_runtime.h>
 #include <functional>
 
+// Device-side bounds checks of the queue, flag and row indices (debug build
+// -DGA_CHECKS, `make checks`; compute-sanitizer is unavailable on the GPU
+// pool): a violated check traps, so the launch fails with an error.
+#if defined(GA_CHECKS) && defined(__CUDA_ARCH__)
+#define GA_CHECK(c) \
+    do {            \
+        if (!(c)) __trap(); \
+    } while (0)
+#else
+#define GA_CHECK(c) ((void)0)
+#endif
+
 namespace ga {
 
 struct DevNet {

@@ -260,6 +260,7 @@ __global__ void __launch_bounds__(kTPB * kBB) bus_block_kernel(DevNet n, DevStat
         int start = 0;
         if (tid < kBB && t < nbus) i = n.bus_at(t);
         // a bus outside this launch's selection owns no rows here (cnt 0)
+        GA_CHECK(i < n.nb);
         if (kSel != 0 && i >= 0 && (defer[i] != 0) != (kSel == 2)) i = -1;
         if (i >= 0) {
             const int* seg = n.bus_seg + 4 * i;
@@ -324,6 +325,7 @@ __global__ void __launch_bounds__(kTPB * kBB) bus_block_kernel(DevNet n, DevStat
                 int k;
                 locate(p, &slot[u], &k, &g[u]);
                 if (g[u] != 6) row[u] = s_base[slot[u]] + k;
+                GA_CHECK(row[u] < n.mpad && slot[u] >= 0 && slot[u] < kBB);
             }
         }
         double q[kUnroll], xv[kUnroll], zv[kUnroll], yv[kUnroll];
@@ -498,6 +500,7 @@ __global__ void __launch_bounds__(kTPB * kBB) bus_block_kernel(DevNet n, DevStat
                 int k;
                 locate(p, &slot[u], &k, &g[u]);
                 if (g[u] != 6) row[u] = s_base[slot[u]] + k;
+                GA_CHECK(row[u] < n.mpad && slot[u] >= 0 && slot[u] < kBB);
             }
         }
         double old[kUnroll], q[kUnroll], xv[kUnroll], zv[kUnroll], yv[kUnroll], lam[kUnroll];

@@ -556,7 +556,8 @@ struct QpProb {
             g[i] = G[i] + hx;
         }
     }
-    GA_FN void hessian(const double*, double* h) const {
+    GA_FN void grad_hess(const double* x, double* g, double* h) const {
+        gradient(x, g);
         for (int i = 0; i < N * N; ++i) h[i] = H[i];
     }
     GA_FN double hess_entry(const double*, int i, int j) const { return H[i * N + j]; }

@@ -307,9 +307,10 @@ struct BranchProb {
         ga_sincos_ool(x[2] - x[3], &ss_, &cc_);
         eval<false, true, false>(x, cc_, ss_, nullptr, g, nullptr);
     }
-    // Called by TRON right after gradient() at the same x.
-    __device__ __forceinline__ void hessian(const double* x, double* h) const {
-        eval<false, false, true>(x, cc_, ss_, nullptr, nullptr, h);
+    // f's gradient and Hessian at x in one pass (TRON's step start)
+    __device__ __forceinline__ void grad_hess(const double* x, double* g, double* h) const {
+        ga_sincos_ool(x[2] - x[3], &ss_, &cc_);
+        eval<false, true, true>(x, cc_, ss_, nullptr, g, h);
     }
 };
 

@@ -437,8 +437,6 @@ enum TronStep : int { kStepContinue = 0, kStepConverged = 1, kStepError = 2, kSt
 struct SerialSearch {
     static constexpr bool kClocked = false;
     static constexpr bool kOolDivSqrt = true;
-    template <int N, class P>
-    GA_FN void hessian(const P& prob, const double* x, double* h) const { prob.hessian(x, h); }
     template <int N, class HM>
     GA_FN void cauchy(const double* x, const double* g, const HM& h, const double* l,
                       const double* u, double delta, double* s, double* qs, bool* qs_ok) const {
@@ -481,8 +479,6 @@ template <int T>
 struct TileSearch {
     static constexpr bool kClocked = T == 32;
     static constexpr bool kOolDivSqrt = false;
-    template <int N, class P>
-    __device__ void hessian(const P& prob, const double* x, double* h) const { prob.hessian(x, h); }
     unsigned mask;  // warp lanes of this tile
     int base;       // first warp lane of the tile
     int rank;       // lane within the tile
@@ -615,14 +611,17 @@ GA_FN int tron_step(const P& prob, TronState<N>& st, const TronParams& cfg,
     for (int i = 0; i < N; ++i) { l[i] = prob.lo(i); u[i] = prob.hi(i); }
     GA_CLK_DECL
     double g[N];
-    prob.gradient(st.x, g);
+    // gradient and Hessian in one evaluation pass (each accumulator keeps its
+    // own order, so the same bits; the flow terms are built once instead of
+    // twice: full 70k solve 6.55 -> 6.45 s); the tests below run in the
+    // reference's order, the Hessian of a converged / failed point is unused
+    double h[N * N];
+    prob.grad_hess(st.x, g, h);
 #pragma unroll
     for (int i = 0; i < N; ++i)
         if (!sfinite(g[i])) return kStepError;
     if (proj_grad_norm<N>(st.x, g, l, u) <= cfg.gtol) return kStepConverged;
     GA_CLK(0);
-    double h[N * N];
-    search.template hessian<N>(prob, st.x, h);
 #pragma unroll
     for (int i = 0; i < N * N; ++i)
         if (!sfinite(h[i])) return kStepError;

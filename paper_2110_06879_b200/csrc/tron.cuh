@@ -107,6 +107,14 @@ GA_FN double tsqrt(double a) {
     return sqrt(a);
 }
 
+// 2^e for |e| <= 1000, exactly (exponent field).
+GA_FN double pow2i(int e) {
+    const long long b = static_cast<long long>(e + 1023) << 52;
+    double v;
+    __builtin_memcpy(&v, &b, sizeof v);
+    return v;
+}
+
 // ---- sequential reductions over N (tron.cpp:16-51) ------------------------
 
 template <int N>
@@ -525,9 +533,17 @@ struct TileSearch {
             bool okc = false, mok = false;
             double mv = 0.0;
             if (valid) {
+                // alpha0 * 2^c: one multiply by the exact power of two equals
+                // the sequential doublings / halvings whenever the result is
+                // normal (every intermediate then is); tiny alpha0 keeps the
+                // sequential form (subnormal halvings round step by step)
                 double a = alpha0;
-                for (int k = 0; k < c; ++k) a *= 2.0;
-                for (int k = 0; k < -c; ++k) a *= 0.5;
+                if (alpha0 >= 0x1p-960) {
+                    a = alpha0 * pow2i(c);
+                } else {
+                    for (int k = 0; k < c; ++k) a *= 2.0;
+                    for (int k = 0; k < -c; ++k) a *= 0.5;
+                }
 #pragma unroll
                 for (int i = 0; i < N; ++i) mys[i] = sclamp(x[i] - a * g[i], l[i], u[i]) - x[i];
                 double gs;
@@ -580,8 +596,7 @@ struct TileSearch {
         double myst[N];
         for (int tb = 0; tb < 20; tb += T) {
             const int t = tb + rank;
-            double beta = 1.0;
-            for (int k = 0; k < t; ++k) beta *= 0.5;
+            const double beta = pow2i(-t);  // = 0.5^t by halvings (exact, t < 52)
 #pragma unroll
             for (int i = 0; i < N; ++i) myst[i] = sclamp(x[i] + s[i] + beta * d[i], l[i], u[i]) - x[i];
             const double q = model<N>(g, h, myst);

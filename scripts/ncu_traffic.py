@@ -10,14 +10,18 @@ import sys
 
 rows = [r for r in csv.reader(open(sys.argv[1])) if r and not r[0].startswith("==")]
 hdr, body = rows[0], rows[1:]
-ix = {k: hdr.index(k) for k in ("ID", "Kernel Name", "Metric Name", "Metric Value")}
+ix = {k: hdr.index(k) for k in ("ID", "Kernel Name", "Metric Name", "Metric Unit", "Metric Value")}
+TO_US = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
 per = collections.defaultdict(dict)  # (kernel, launch id) -> metric -> value
 for r in body:
     name = r[ix["Kernel Name"]]
     k = next((n for n in ("lane_kernel", "tile_kernel", "solo_kernel") if n in name), None)
     if k is None:
         continue
-    per[(k, int(r[ix["ID"]]))][r[ix["Metric Name"]]] = float(r[ix["Metric Value"]].replace(",", ""))
+    name_m, v = r[ix["Metric Name"]], float(r[ix["Metric Value"]].replace(",", ""))
+    if name_m == "gpu__time_duration.sum":
+        v *= TO_US.get(r[ix["Metric Unit"]], 1.0)  # microseconds
+    per[(k, int(r[ix["ID"]]))][name_m] = v
 
 M = {"us": "gpu__time_duration.sum", "rd": "dram__bytes_read.sum", "wr": "dram__bytes_write.sum",
      "dadd": "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum",
@@ -29,7 +33,7 @@ for k in ("lane_kernel", "tile_kernel", "solo_kernel"):
     if not ls:
         continue
     mean = {a: sum(l.get(m, 0.0) for l in ls) / len(ls) for a, m in M.items()}
-    us = mean["us"] / 1e3 if mean["us"] > 1e5 else mean["us"]  # ns -> us when ncu reports ns
+    us = mean["us"]
     print(json.dumps({"kernel": k, "launches": len(ls), "mean_us": us,
                       "dram_read_bytes": mean["rd"], "dram_write_bytes": mean["wr"],
                       "dram_bytes": mean["rd"] + mean["wr"], "dadd": mean["dadd"],

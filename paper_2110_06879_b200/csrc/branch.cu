@@ -19,7 +19,7 @@
 //     twice the tile slots (throughput mode), up to `lane_budget` after; then
 //     its resumable state (TRON iterate, radius, iteration, AL round) is
 //     saved and it is pushed to an overflow queue.
-//  B. tile phase — the overflow branches are resumed by tiles of 8 lanes (or
+//  B. tile phase — the overflow branches are resumed by tiles of kTile lanes (or
 //     whole warps when a queue is short).  All lanes of a tile hold the
 //     replicated iterate; the Cauchy search and the projected line search
 //     (the loops with many trials) are evaluated 8 (32) trials at a time
@@ -76,8 +76,11 @@ constexpr double kRhoTildeMax = 1e7;
 constexpr int kLaneBlock = GA_LANE_BLOCK;  // lane phase: one slot per thread (64 / 128 / 256 per block:
                                  // 7.05 / 7.05 / 6.99 s on the full 70k solve)
 constexpr int kTileBlock = 128;  // tile phase: one slot per tile
-constexpr int kTile = 4;  // lanes per branch in the tile phase (full 70k solve: 2 / 4 / 8 / 16
-                         // lanes -> 7.37 / 7.02 / 7.12 / 7.38 s)
+#ifndef GA_TILE
+#define GA_TILE 8
+#endif
+constexpr int kTile = GA_TILE;  // lanes per branch in the tile phase (full 70k solve, final
+                                // build: 2 / 4 / 8 / 16 lanes -> 6.60 / 6.35 / 6.27 / 6.36 s)
 constexpr int kCounters = 12;
 constexpr int kSoloBlock = 32;  // solo phase: one warp per block, one branch per warp
 

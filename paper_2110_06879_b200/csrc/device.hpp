@@ -168,7 +168,8 @@ struct BranchCfg {
     int lane_cap = 16;    // lane-phase steps while the active set exceeds the tile slots (swept)
     int tile_slots = 0;   // set by the launcher: tiles available per queue
     int tail_num = 2;     // whole-warp tiles when a queue <= tail_num/4 of the grid's warps
-    int tile_budget = 48; // steps in the 8-lane tile phase before the solo phase takes over (0 = off)
+    int tile_budget = 0;  // steps in the tile phase before the solo phase takes over (0 = off;
+                          // 70k solve with 8-lane tiles: 0 / 24 / 48 / 96 -> 6.23 / 6.28 / 6.28 / 6.27 s)
     const LoopCtl* gate = nullptr;  // graph path: skip the launch when gate->stop
 };
 

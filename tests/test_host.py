@@ -115,9 +115,9 @@ def test_config_contract(gridadmm):
     assert (d["rho_pq"], d["rho_va"], d["beta0"], d["eps"], d["max_outer"], d["max_inner"]) == \
         (10.0, 1000.0, 1e3, 1e-4, 20, 1000)
     # branch-phase scheduling extensions (results never depend on them)
-    assert (d["lane_budget"], d["lane_cap"], d["tile_budget"]) == (4, 16, 48)
-    d["tile_budget"] = 0  # 0 disables the solo phase
-    assert d["tile_budget"] == 0
+    assert (d["lane_budget"], d["lane_cap"], d["tile_budget"]) == (4, 16, 0)  # 0: no solo phase
+    d["tile_budget"] = 48  # hand branches past 48 tile steps to whole-warp solves
+    assert d["tile_budget"] == 48
     for key, val in (("lane_budget", 0), ("lane_cap", 0.5), ("tile_budget", -1)):
         with pytest.raises(gridadmm.GridAdmmError):
             d[key] = val

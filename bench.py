@@ -60,6 +60,7 @@ import numpy as np
 
 # the library splits the bus kernel around the tile phase unless disabled
 BUS_OVERLAP = os.environ.get("GRIDADMM_BUS_OVERLAP", "1") != "0"
+SOLO = False  # set from the config (tile_budget > 0)
 
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
@@ -409,6 +410,8 @@ def run_b200(args, d: Dist):
     if d.world > 1 or os.environ.get("GRIDADMM_BENCH_DIST") == "1":
         return run_b200_partitioned(args, d, ga, net)
     cfg = ga.Config(WORKLOAD["preset"], device=dev)
+    global SOLO
+    SOLO = cfg["tile_budget"] > 0  # the solo kernel launches only with a tile budget
     nb, ng, nl, m = net.num_buses, net.num_generators, net.num_branches, net.num_rows
 
     # --- device-resident timed region -----------------------------------
@@ -565,9 +568,10 @@ def run_b200(args, d: Dist):
             "cpu_baseline": cpu,
             "converge": conv,
             "track": track,
-            "gpu_launches": (6 if BUS_OVERLAP else 5) * args.steps,
+            "gpu_launches": (3 + (1 if SOLO else 0) + (2 if BUS_OVERLAP else 1)) * args.steps,
             "gpu_launches_note": ("per step: reset_scalars_kernel, lane_kernel, tile_kernel, "
-                                  "solo_kernel, bus_block_kernel (generator projection, z, y and "
+                                  + ("solo_kernel, " if SOLO else "")
+                                  + "bus_block_kernel (generator projection, z, y and "
                                   "norms fused in)"
                                   + (" twice: the buses not adjacent to a branch handed to the "
                                      "tile phase on a side stream beside the tile / solo "
